@@ -1,0 +1,150 @@
+/*
+ * cerdot — B200 (sm_100a) CER/CSER conversion and dot product, C ABI.
+ *
+ * The reference (`lemt`, pure Python) has no FFI; its drop-in boundary is the
+ * module-level Python API.  Each entry point below replaces the numpy body of
+ * one reference function and is bound from Python with ctypes by
+ * paper_1805_10692_b200/_native.py (see INTEGRATION.md for the binding a
+ * maintainer would add to lemt itself):
+ *
+ *   cerdot_encode_plan / cerdot_encode_fill
+ *       replace lemt.formats._frequency_alphabet + _segment_layout +
+ *       encode_cer / encode_cser                (formats.py:193-295)
+ *   cerdot_dot / cerdot_dot_cer / cerdot_dot_cser
+ *       replace lemt.kernels._dot_segmented + dot_cer / dot_cser / dot
+ *                                               (kernels.py:283-336)
+ *   cerdot_index_bitwidth
+ *       replaces lemt.formats.index_bitwidth     (formats.py:52-59)
+ *   cerdot_shard_plan
+ *       new: contiguous row blocks balanced by encoded bytes
+ *
+ * Conventions
+ *   - Every pointer marked (device) is CUDA device memory on the current
+ *     device; every size is in elements unless named *_bytes.
+ *   - The caller allocates every buffer (sizes come from the plan); the
+ *     library never allocates or frees caller memory and keeps no global
+ *     mutable state besides a per-thread last-error string.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  All device
+ *     work is stream-ordered.  cerdot_encode_plan synchronises `stream`
+ *     (its outputs are sizes the caller needs to allocate); nothing else does.
+ *   - Status codes map 1:1 onto the reference's Python exceptions:
+ *       CERDOT_E_VALUE -> ValueError   (formats.py:54-71, kernels.py:106-110)
+ *       CERDOT_E_TYPE  -> TypeError    (kernels.py:336)
+ *       CERDOT_E_INDEX -> IndexError   (empty alphabet, formats.py:199)
+ *       CERDOT_E_CUDA / CERDOT_E_UNSUPPORTED -> RuntimeError
+ *     cerdot_last_error() returns the message for the calling thread.
+ */
+#ifndef CERDOT_H_
+#define CERDOT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CERDOT_ABI_VERSION 1
+
+typedef enum {
+  CERDOT_OK = 0,
+  CERDOT_E_VALUE = 1,
+  CERDOT_E_TYPE = 2,
+  CERDOT_E_INDEX = 3,
+  CERDOT_E_CUDA = 4,
+  CERDOT_E_UNSUPPORTED = 5,
+  CERDOT_E_WORKSPACE = 6 /* workspace too small: info->workspace_bytes holds the need */
+} cerdot_status;
+
+typedef enum { CERDOT_CER = 0, CERDOT_CSER = 1 } cerdot_kind;
+typedef enum { CERDOT_F32 = 0, CERDOT_F64 = 1 } cerdot_dtype;
+
+/* A CER or CSER matrix resident in device memory (field meaning as
+ * lemt.formats.CerMatrix / CserMatrix, formats.py:105-170). */
+typedef struct {
+  int32_t kind;               /* cerdot_kind */
+  int32_t mode_index;         /* CSER: position of the background in omega; CER: 0 */
+  int64_t m, n;               /* rows, columns */
+  int64_t k;                  /* alphabet size, len(omega) */
+  int64_t nnz;                /* len(col_index) */
+  int64_t segments;           /* len(omega_ptr) - 1 */
+  const double *omega;        /* (device) k: CER frequency-major, CSER value-ascending */
+  const void *col_index;      /* (device) nnz unsigned ints of col_bits */
+  const void *omega_ptr;      /* (device) segments+1 unsigned ints of omega_ptr_bits */
+  const void *row_ptr;        /* (device) m+1 unsigned ints of row_ptr_bits */
+  const void *omega_index;    /* (device) CSER: segments unsigned ints of omega_index_bits */
+  int32_t col_bits, omega_ptr_bits, row_ptr_bits, omega_index_bits; /* 8, 16 or 32 */
+  double background;          /* host copy of omega[0] (CER) / omega[mode_index] (CSER) */
+} cerdot_matrix;
+
+/* Result of phase 1 of the conversion. */
+typedef struct {
+  int64_t m, n;
+  int64_t k;                  /* alphabet size (a prepended absent background included) */
+  int64_t nnz;                /* non-background entries */
+  int64_t segments_cer;       /* CER segments incl. empty padding */
+  int64_t segments_cser;      /* CSER segments (present elements only) */
+  int32_t mode_index;         /* CSER position of the background */
+  int32_t path;               /* 0 = on-chip hash path (k <= CERDOT_FAST_K), 1 = sort path */
+  double background;          /* omega[0] of the CER alphabet */
+  size_t workspace_bytes;     /* bytes of workspace the plan+fill need */
+} cerdot_encode_info;
+
+#define CERDOT_FAST_K 2048
+
+int cerdot_abi_version(void);
+const char *cerdot_last_error(void);
+
+/* Smallest of 8/16/32 holding max_value unsigned, or 0 with CERDOT_E_VALUE set
+ * when max_value is negative or needs more than 32 bits (formats.py:52-59). */
+int32_t cerdot_index_bitwidth(int64_t max_value);
+
+/* Workspace bound for the on-chip path of an m x n matrix.  Call the plan with
+ * at least this; the plan reports a larger need (CERDOT_E_WORKSPACE) only
+ * when the alphabet is too large for the on-chip path. */
+size_t cerdot_encode_workspace_bytes(int64_t m, int64_t n);
+
+/* Phase 1: alphabet, ranks, per-row counts, sizes.
+ *   w        (device) m x n values, row stride ldw elements, dtype f32 or f64
+ *   bg_mode  0: background = most frequent value (ties -> smallest);
+ *            1: background = bg_value (prepended when absent)  (formats.py:198-205)
+ * Synchronises `stream`; fills *info.  The workspace holds the state the fill
+ * reads, so do not reuse it in between. */
+int cerdot_encode_plan(const void *w, int32_t dtype, int64_t m, int64_t n, int64_t ldw, int32_t bg_mode,
+                       double bg_value, void *workspace, size_t workspace_bytes, cerdot_encode_info *info,
+                       void *stream);
+
+/* Phase 2: write one encoding into caller buffers sized from *info:
+ *   omega k doubles; col_index nnz; omega_ptr S+1; row_ptr m+1; omega_index S (CSER)
+ * with S = segments_cer / segments_cser.  Widths are 8/16/32 and must hold the
+ * largest value (formats.py:66-74); CERDOT_E_VALUE otherwise. */
+int cerdot_encode_fill(const cerdot_encode_info *info, int32_t kind, void *workspace, size_t workspace_bytes,
+                       double *omega, void *col_index, int32_t col_bits, void *omega_ptr, int32_t omega_ptr_bits,
+                       void *row_ptr, int32_t row_ptr_bits, void *omega_index, int32_t omega_index_bits,
+                       void *stream);
+
+/* Workspace the dot needs (zero unless the background is non-zero: then
+ * batch doubles for the column sums of x). */
+size_t cerdot_dot_workspace_bytes(const cerdot_matrix *a, int64_t batch);
+
+/* y (m x batch, row stride ldy) = A . x (n x batch, row stride ldx), fp32.
+ * batch == 1 is the mat-vec.  Stream-ordered, no allocation, deterministic. */
+int cerdot_dot(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,
+               void *workspace, size_t workspace_bytes, void *stream);
+int cerdot_dot_cer(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,
+                   void *workspace, size_t workspace_bytes, void *stream);
+int cerdot_dot_cser(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,
+                    void *workspace, size_t workspace_bytes, void *stream);
+
+/* Row-shard planner (host).  row_ptr / omega_ptr are HOST arrays of the
+ * given widths.  Writes parts+1 row bounds (bounds[0]=0, bounds[parts]=m)
+ * splitting rows into contiguous blocks of near-equal encoded bytes
+ * (entries*col_bytes + segments*ptr_bytes + rows*row_bytes). */
+int cerdot_shard_plan(const void *row_ptr, int32_t row_ptr_bits, const void *omega_ptr, int32_t omega_ptr_bits,
+                      int32_t col_bits, int64_t m, int32_t parts, int64_t *bounds);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CERDOT_H_ */

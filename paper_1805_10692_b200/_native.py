@@ -1,0 +1,125 @@
+"""ctypes binding of libcerdot (include/cerdot.h).
+
+The library is the product: there is no CPU fallback.  Loading fails loudly
+when the shared object is missing, and every call that needs a GPU fails
+loudly when CUDA is unavailable.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+LIB_PATH = os.path.join(PKG, "_lib", "libcerdot.so")
+HEADER = os.path.join(ROOT, "include", "cerdot.h")
+
+OK, E_VALUE, E_TYPE, E_INDEX, E_CUDA, E_UNSUPPORTED, E_WORKSPACE = range(7)
+CER, CSER = 0, 1
+F32, F64 = 0, 1
+FAST_K = 2048
+
+
+class CerdotMatrix(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("mode_index", ctypes.c_int32),
+        ("m", ctypes.c_int64),
+        ("n", ctypes.c_int64),
+        ("k", ctypes.c_int64),
+        ("nnz", ctypes.c_int64),
+        ("segments", ctypes.c_int64),
+        ("omega", ctypes.c_void_p),
+        ("col_index", ctypes.c_void_p),
+        ("omega_ptr", ctypes.c_void_p),
+        ("row_ptr", ctypes.c_void_p),
+        ("omega_index", ctypes.c_void_p),
+        ("col_bits", ctypes.c_int32),
+        ("omega_ptr_bits", ctypes.c_int32),
+        ("row_ptr_bits", ctypes.c_int32),
+        ("omega_index_bits", ctypes.c_int32),
+        ("background", ctypes.c_double),
+    ]
+
+
+class CerdotEncodeInfo(ctypes.Structure):
+    _fields_ = [
+        ("m", ctypes.c_int64),
+        ("n", ctypes.c_int64),
+        ("k", ctypes.c_int64),
+        ("nnz", ctypes.c_int64),
+        ("segments_cer", ctypes.c_int64),
+        ("segments_cser", ctypes.c_int64),
+        ("mode_index", ctypes.c_int32),
+        ("path", ctypes.c_int32),
+        ("background", ctypes.c_double),
+        ("workspace_bytes", ctypes.c_size_t),
+    ]
+
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_SZ = ctypes.c_size_t
+_SIGNATURES = {
+    "cerdot_abi_version": (ctypes.c_int, []),
+    "cerdot_last_error": (ctypes.c_char_p, []),
+    "cerdot_index_bitwidth": (_I32, [_I64]),
+    "cerdot_encode_workspace_bytes": (_SZ, [_I64, _I64]),
+    "cerdot_encode_plan": (ctypes.c_int, [_P, _I32, _I64, _I64, _I64, _I32, ctypes.c_double, _P, _SZ,
+                                          ctypes.POINTER(CerdotEncodeInfo), _P]),
+    "cerdot_encode_fill": (ctypes.c_int, [ctypes.POINTER(CerdotEncodeInfo), _I32, _P, _SZ, _P, _P, _I32, _P, _I32,
+                                          _P, _I32, _P, _I32, _P]),
+    "cerdot_dot_workspace_bytes": (_SZ, [ctypes.POINTER(CerdotMatrix), _I64]),
+    "cerdot_dot": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _SZ, _P]),
+    "cerdot_dot_cer": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _SZ, _P]),
+    "cerdot_dot_cser": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _SZ, _P]),
+    "cerdot_shard_plan": (ctypes.c_int, [_P, _I32, _P, _I32, _I32, _I64, _I32, ctypes.POINTER(ctypes.c_int64)]),
+}
+
+_lib = None
+
+
+def header_functions() -> list[str]:
+    """Every function the public header declares (used by the export test)."""
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(cerdot_\w+)\s*\(", text, flags=re.M)))
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"libcerdot.so not found at {LIB_PATH}; build it with `python -m paper_1805_10692_b200.build` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        if L.cerdot_abi_version() != 1:
+            raise ImportError("libcerdot ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    msg = lib().cerdot_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int) -> None:
+    """Map a status code onto the reference's exception types."""
+    if status == OK:
+        return
+    msg = last_error()
+    if status == E_VALUE:
+        raise ValueError(msg)
+    if status == E_TYPE:
+        raise TypeError(msg)
+    if status == E_INDEX:
+        raise IndexError(msg)
+    raise RuntimeError(f"libcerdot: {msg} (status {status})")

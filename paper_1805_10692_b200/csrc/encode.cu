@@ -1,0 +1,668 @@
+// Dense -> CER / CSER conversion on sm_100a (bit-exact with lemt.formats).
+//
+// Reference: lemt formats.py:193-295.  The reference sorts every element
+// (np.unique + lexsort over (row, rank, col)); here the work is split into
+// streaming passes that each read the matrix (or its 1-2 byte rank grid) once:
+//
+//   k_value_hist    value histogram: per-CTA shared-memory hash table with
+//                   warp-aggregated (match.any) counting, merged into a small
+//                   global table                         (formats.py:195)
+//   k_alphabet      one CTA: (count desc, value asc) order, background moved
+//                   or prepended, value-ascending positions for CSER, and the
+//                   value -> rank lookup table            (formats.py:196-208, 269-271)
+//   k_row_count     CTA per row: rank of every element (rank grid), per-row
+//                   non-background count, last present rank, present count
+//                                                         (formats.py:218-223, 238-240, 274-278)
+//   k_scan_rows     exclusive scans -> entry offsets, CER/CSER row pointers
+//                                                         (formats.py:246-247, 283-284)
+//   k_row_fill      CTA per row: per-rank block scan -> omegaPtr (+ omegaI),
+//                   then a stable per-warp-slab counting scatter of the
+//                   columns into colI: (row, rank, col) order without a sort
+//                                                         (formats.py:220-221, 241-247, 273-283)
+//
+// Alphabets larger than CERDOT_FAST_K take CERDOT_E_UNSUPPORTED for now
+// (reported back as RuntimeError by the Python layer).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+
+#include "common.cuh"
+#include "encode.cuh"
+
+namespace cerdot {
+
+namespace {
+
+constexpr int kLocalCap = 2048;        // per-CTA hash slots in k_value_hist
+constexpr int kLocalProbe = 64;        // probes before spilling to the global table
+constexpr int kGlobalCap = 8192;       // global hash slots (<= 25% load at the fast limit)
+constexpr int kFastDistinct = CERDOT_FAST_K - 1;  // room for a prepended background
+constexpr int kRowThreads = 256;
+constexpr int kRowWarps = kRowThreads / 32;
+
+struct Ctrl {
+  unsigned int distinct;     // distinct keys inserted in the global table
+  unsigned int overflow;     // alphabet exceeds the on-chip path
+  unsigned int pos_zero;     // a +0.0 was seen
+  unsigned int neg_zero;     // a -0.0 was seen
+  unsigned int k;            // final alphabet size
+  unsigned int rcap;         // rank table capacity (power of two)
+  int mode_index;            // CSER background position
+  int pad;
+  double background;         // omega[0]
+};
+
+struct FastWs {
+  unsigned long long *gkey;   // kGlobalCap
+  unsigned long long *gcnt;   // kGlobalCap
+  double *omega_freq;         // CERDOT_FAST_K
+  uint32_t *to_vpos;          // CERDOT_FAST_K
+  unsigned long long *rkey;   // 2 * CERDOT_FAST_K
+  uint32_t *rrank;            // 2 * CERDOT_FAST_K
+  Ctrl *ctrl;
+  uint64_t *row_stat;         // 3*m: nnz, last, present
+  uint64_t *scan;             // 3*(m+1): entry offset, CER row ptr, CSER row ptr
+  void *ranks;                // m*n rank grid (u8 if k <= 256 else u16)
+  size_t bytes;
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+FastWs carve(void *base, int64_t m, int64_t n) {
+  FastWs w{};
+  char *p = static_cast<char *>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    void *r = p ? p + off : nullptr;
+    off = align_up(off + bytes, 256);
+    return r;
+  };
+  w.gkey = static_cast<unsigned long long *>(take(sizeof(unsigned long long) * kGlobalCap));
+  w.gcnt = static_cast<unsigned long long *>(take(sizeof(unsigned long long) * kGlobalCap));
+  w.omega_freq = static_cast<double *>(take(sizeof(double) * CERDOT_FAST_K));
+  w.to_vpos = static_cast<uint32_t *>(take(sizeof(uint32_t) * CERDOT_FAST_K));
+  w.rkey = static_cast<unsigned long long *>(take(sizeof(unsigned long long) * 2 * CERDOT_FAST_K));
+  w.rrank = static_cast<uint32_t *>(take(sizeof(uint32_t) * 2 * CERDOT_FAST_K));
+  w.ctrl = static_cast<Ctrl *>(take(sizeof(Ctrl)));
+  w.row_stat = static_cast<uint64_t *>(take(sizeof(uint64_t) * 3 * m));
+  w.scan = static_cast<uint64_t *>(take(sizeof(uint64_t) * 3 * (m + 1)));
+  w.ranks = take(static_cast<size_t>(m) * n * 2);
+  w.bytes = off;
+  return w;
+}
+
+// ---------------------------------------------------------------- hashing
+__device__ __forceinline__ bool global_insert(unsigned long long *gkey, unsigned long long *gcnt, Ctrl *ctrl,
+                                              unsigned long long key, unsigned long long cnt) {
+  uint32_t h = hash_key(key) & (kGlobalCap - 1);
+  for (int probe = 0; probe < kGlobalCap; ++probe) {
+    unsigned long long cur = gkey[h];
+    if (cur == kEmptyKey) {
+      if (ctrl->distinct >= kFastDistinct) {
+        atomicOr(&ctrl->overflow, 1u);
+        return false;
+      }
+      cur = atomicCAS(&gkey[h], kEmptyKey, key);
+      if (cur == kEmptyKey) {
+        if (atomicAdd(&ctrl->distinct, 1u) >= kFastDistinct) atomicOr(&ctrl->overflow, 1u);
+        cur = key;
+      }
+    }
+    if (cur == key) {
+      atomicAdd(&gcnt[h], cnt);
+      return true;
+    }
+    h = (h + 1) & (kGlobalCap - 1);
+  }
+  atomicOr(&ctrl->overflow, 1u);
+  return false;
+}
+
+template <typename T, int V>
+struct VecLoad;
+template <>
+struct VecLoad<float, 4> {
+  __device__ static void load(const float *p, double (&out)[4]) {
+    float4 v = __ldg(reinterpret_cast<const float4 *>(p));
+    out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+  }
+};
+template <>
+struct VecLoad<double, 2> {
+  __device__ static void load(const double *p, double (&out)[2]) {
+    double2 v = __ldg(reinterpret_cast<const double2 *>(p));
+    out[0] = v.x; out[1] = v.y;
+  }
+};
+
+// V elements per lane per step; V > 1 requires a contiguous, 16B-aligned matrix.
+template <typename T, int V>
+__global__ void __launch_bounds__(256) k_value_hist(const T *__restrict__ w, int64_t m, int64_t n, int64_t ldw,
+                                                    FastWs ws) {
+  __shared__ unsigned long long skey[kLocalCap];
+  __shared__ unsigned int scnt[kLocalCap];
+  for (int i = threadIdx.x; i < kLocalCap; i += blockDim.x) {
+    skey[i] = kEmptyKey;
+    scnt[i] = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t total = m * n;
+  const bool contig = (ldw == n);
+  const int64_t nvec = ceil_div(total, V);
+  const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  unsigned int saw_pos0 = 0, saw_neg0 = 0;
+  for (int64_t base = warp_id * 32; base < nvec; base += nwarps * 32) {
+    const int64_t vi = base + lane;
+    double vals[V];
+    bool valid[V];
+    if (V > 1 && vi * V + V <= total) {
+      double tmp[V];
+      if constexpr (V > 1) VecLoad<T, V>::load(w + vi * V, tmp);
+#pragma unroll
+      for (int j = 0; j < V; ++j) { vals[j] = tmp[j]; valid[j] = true; }
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int64_t e = vi * V + j;
+        valid[j] = e < total;
+        if (valid[j]) {
+          int64_t addr = e;
+          if (!contig) {
+            const int64_t r = e / n;
+            addr = r * ldw + (e - r * n);
+          }
+          vals[j] = as_double(__ldg(w + addr));
+        } else {
+          vals[j] = 0.0;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const unsigned long long key = valid[j] ? value_key(vals[j]) : kEmptyKey;
+      if (valid[j] && vals[j] == 0.0) {
+        if (__double_as_longlong(vals[j]) < 0) saw_neg0 = 1; else saw_pos0 = 1;
+      }
+      const unsigned int peers = __match_any_sync(0xffffffffu, key);
+      if (key != kEmptyKey && lane == __ffs(peers) - 1) {
+        const unsigned int cnt = __popc(peers);
+        uint32_t h = hash_key(key) & (kLocalCap - 1);
+        bool done = false;
+        for (int probe = 0; probe < kLocalProbe; ++probe) {
+          unsigned long long cur = skey[h];
+          if (cur == kEmptyKey) cur = atomicCAS(&skey[h], kEmptyKey, key), cur = (cur == kEmptyKey) ? key : cur;
+          if (cur == key) {
+            atomicAdd(&scnt[h], cnt);
+            done = true;
+            break;
+          }
+          h = (h + 1) & (kLocalCap - 1);
+        }
+        if (!done) global_insert(ws.gkey, ws.gcnt, ws.ctrl, key, cnt);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, saw_pos0) && lane == 0) atomicOr(&ws.ctrl->pos_zero, 1u);
+  if (__any_sync(0xffffffffu, saw_neg0) && lane == 0) atomicOr(&ws.ctrl->neg_zero, 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kLocalCap; i += blockDim.x)
+    if (skey[i] != kEmptyKey) global_insert(ws.gkey, ws.gcnt, ws.ctrl, skey[i], scnt[i]);
+}
+
+// One CTA: order the alphabet and build the rank lookup table.
+__global__ void __launch_bounds__(1024) k_alphabet(FastWs ws, int bg_mode, double bg_value) {
+  __shared__ unsigned long long key[CERDOT_FAST_K];
+  __shared__ unsigned long long cnt[CERDOT_FAST_K];
+  __shared__ unsigned int final_rank[CERDOT_FAST_K];  // by compacted index
+  __shared__ unsigned int n_distinct;
+  __shared__ int bg_pos;                              // frequency position of the background, -1 if absent
+  __shared__ unsigned int k_final, rcap;
+  Ctrl *ctrl = ws.ctrl;
+  if (threadIdx.x == 0) {
+    n_distinct = 0;
+    bg_pos = -1;
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < kGlobalCap; s += blockDim.x) {
+    const unsigned long long kk = ws.gkey[s];
+    if (kk != kEmptyKey) {
+      const unsigned int idx = atomicAdd(&n_distinct, 1u);
+      key[idx] = kk;
+      cnt[idx] = ws.gcnt[s];
+    }
+  }
+  __syncthreads();
+  const int k0 = static_cast<int>(n_distinct);
+  const unsigned long long bg_key_explicit = value_key(bg_value);
+  // frequency position: count desc, value (key) asc -- a total order on distinct keys
+  for (int i = threadIdx.x; i < k0; i += blockDim.x) {
+    int r = 0;
+    const unsigned long long ci = cnt[i], ki = key[i];
+    for (int j = 0; j < k0; ++j) r += (cnt[j] > ci) || (cnt[j] == ci && key[j] < ki);
+    final_rank[i] = r;
+    if (bg_mode ? (ki == bg_key_explicit) : (r == 0)) bg_pos = r;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    k_final = bg_pos >= 0 ? k0 : k0 + 1;
+    unsigned int c = 64;
+    while (c < 2 * k_final) c <<= 1;
+    rcap = c;
+  }
+  __syncthreads();
+  const int kf = static_cast<int>(k_final);
+  const int bp = bg_pos;
+  // move / prepend the background (formats.py:201-205)
+  for (int i = threadIdx.x; i < k0; i += blockDim.x) {
+    const int r = static_cast<int>(final_rank[i]);
+    final_rank[i] = bp < 0 ? r + 1 : (r == bp ? 0 : (r < bp ? r + 1 : r));
+  }
+  for (int s = threadIdx.x; s < static_cast<int>(rcap); s += blockDim.x) ws.rkey[s] = kEmptyKey;
+  __syncthreads();
+  for (int i = threadIdx.x; i < k0; i += blockDim.x) {
+    const int f = static_cast<int>(final_rank[i]);
+    double v = key_value(key[i]);
+    if (v == 0.0) v = ctrl->pos_zero ? 0.0 : -0.0;  // np.unique keeps one zero; see DESIGN.md
+    if (f == 0 && bg_mode) v = bg_value;              // the given background heads omega as given
+    ws.omega_freq[f] = v;
+    // rank lookup table
+    uint32_t h = hash_key(key[i]) & (rcap - 1);
+    while (atomicCAS(&ws.rkey[h], kEmptyKey, key[i]) != kEmptyKey) h = (h + 1) & (rcap - 1);
+    ws.rrank[h] = static_cast<uint32_t>(f);
+  }
+  if (bp < 0 && threadIdx.x == 0) ws.omega_freq[0] = bg_value;
+  __syncthreads();
+  // value-ascending position of every final element (CSER, formats.py:269-270)
+  for (int f = threadIdx.x; f < kf; f += blockDim.x) {
+    const unsigned long long kf_key = value_key(ws.omega_freq[f]);
+    int pos = 0;
+    for (int g = 0; g < kf; ++g) pos += value_key(ws.omega_freq[g]) < kf_key;
+    ws.to_vpos[f] = pos;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctrl->k = k_final;
+    ctrl->rcap = rcap;
+    ctrl->mode_index = static_cast<int>(ws.to_vpos[0]);
+    ctrl->background = ws.omega_freq[0];
+  }
+}
+
+__device__ __forceinline__ void block_reduce3(uint64_t &a, uint64_t &b, uint64_t &c, uint64_t *sh) {
+  // a, b: sums; c: max.  sh holds 3*32 entries.
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c = max(c, __shfl_xor_sync(0xffffffffu, c, o));
+  }
+  __syncthreads();
+  if (lane == 0) {
+    sh[wid] = a;
+    sh[32 + wid] = b;
+    sh[64 + wid] = c;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    a = lane < nw ? sh[lane] : 0;
+    b = lane < nw ? sh[32 + lane] : 0;
+    c = lane < nw ? sh[64 + lane] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      c = max(c, __shfl_xor_sync(0xffffffffu, c, o));
+    }
+  }
+}
+
+// CTA per row: ranks + per-row statistics.
+template <typename T, typename RankT>
+__global__ void __launch_bounds__(kRowThreads) k_row_count(const T *__restrict__ w, int64_t m, int64_t n,
+                                                           int64_t ldw, FastWs ws) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint64_t red[96];
+  const unsigned int rcap = ws.ctrl->rcap;
+  const unsigned int k = ws.ctrl->k;
+  unsigned long long *rkey = reinterpret_cast<unsigned long long *>(smem);
+  unsigned int *hist = reinterpret_cast<unsigned int *>(rkey + rcap);
+  unsigned short *rrank = reinterpret_cast<unsigned short *>(hist + k);
+  for (unsigned int s = threadIdx.x; s < rcap; s += blockDim.x) {
+    rkey[s] = ws.rkey[s];
+    rrank[s] = static_cast<unsigned short>(ws.rrank[s]);
+  }
+  RankT *ranks = static_cast<RankT *>(ws.ranks);
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+    for (unsigned int q = threadIdx.x; q < k; q += blockDim.x) hist[q] = 0;
+    __syncthreads();
+    const T *wr = w + row * ldw;
+    RankT *rr = ranks + row * n;
+    for (int64_t c0 = threadIdx.x - lane; c0 < n; c0 += blockDim.x) {
+      const int64_t c = c0 + lane;
+      unsigned int rk = 0;
+      if (c < n) {
+        const unsigned long long kk = value_key(as_double(__ldg(wr + c)));
+        uint32_t h = hash_key(kk) & (rcap - 1);
+        while (rkey[h] != kk) h = (h + 1) & (rcap - 1);
+        rk = rrank[h];
+        rr[c] = static_cast<RankT>(rk);
+      }
+      const unsigned int peers = __match_any_sync(0xffffffffu, rk);
+      if (rk != 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[rk], __popc(peers));
+    }
+    __syncthreads();
+    uint64_t nnz = 0, present = 0, last = 0;
+    for (unsigned int q = 1 + threadIdx.x; q < k; q += blockDim.x) {
+      const unsigned int h = hist[q];
+      nnz += h;
+      present += h > 0;
+      if (h) last = max(last, static_cast<uint64_t>(q));
+    }
+    block_reduce3(nnz, present, last, red);
+    if (threadIdx.x == 0) {
+      ws.row_stat[row] = nnz;
+      ws.row_stat[m + row] = last;
+      ws.row_stat[2 * m + row] = present;
+    }
+    __syncthreads();
+  }
+}
+
+// One CTA of 1024 threads: three exclusive scans over m rows (m+1 outputs each).
+__global__ void __launch_bounds__(1024) k_scan_rows(int64_t m, FastWs ws) {
+  __shared__ uint64_t part[3][1024];
+  const int t = threadIdx.x;
+  const int64_t per = ceil_div(m, 1024);
+  const int64_t r0 = min64(m, t * per), r1 = min64(m, r0 + per);
+  uint64_t s[3] = {0, 0, 0};
+  for (int64_t r = r0; r < r1; ++r)
+    for (int j = 0; j < 3; ++j) s[j] += ws.row_stat[j * m + r];
+  for (int j = 0; j < 3; ++j) part[j][t] = s[j];
+  __syncthreads();
+  // Hillis-Steele inclusive scan on 1024 partials (tiny)
+  for (int off = 1; off < 1024; off <<= 1) {
+    uint64_t v[3];
+    for (int j = 0; j < 3; ++j) v[j] = t >= off ? part[j][t - off] : 0;
+    __syncthreads();
+    for (int j = 0; j < 3; ++j) part[j][t] += v[j];
+    __syncthreads();
+  }
+  uint64_t run[3];
+  for (int j = 0; j < 3; ++j) run[j] = part[j][t] - s[j];
+  for (int64_t r = r0; r < r1; ++r)
+    for (int j = 0; j < 3; ++j) {
+      ws.scan[j * (m + 1) + r] = run[j];
+      run[j] += ws.row_stat[j * m + r];
+    }
+  if (t == 1023)
+    for (int j = 0; j < 3; ++j) ws.scan[j * (m + 1) + m] = part[j][1023];
+}
+
+// Exclusive block scan of (a, b) pairs over the CTA; returns totals too.
+__device__ __forceinline__ void block_exscan2(unsigned int a, unsigned int b, unsigned int &ea, unsigned int &eb,
+                                              unsigned int *sh /* 2*32 */) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned int ia = a, ib = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned int va = __shfl_up_sync(0xffffffffu, ia, o);
+    const unsigned int vb = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) { ia += va; ib += vb; }
+  }
+  if (lane == 31) { sh[wid] = ia; sh[32 + wid] = ib; }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    unsigned int wa = lane < nw ? sh[lane] : 0, wb = lane < nw ? sh[32 + lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned int va = __shfl_up_sync(0xffffffffu, wa, o);
+      const unsigned int vb = __shfl_up_sync(0xffffffffu, wb, o);
+      if (lane >= o) { wa += va; wb += vb; }
+    }
+    sh[lane] = wa;
+    sh[32 + lane] = wb;
+  }
+  __syncthreads();
+  const unsigned int base_a = wid ? sh[wid - 1] : 0, base_b = wid ? sh[32 + wid - 1] : 0;
+  ea = base_a + ia - a;
+  eb = base_b + ib - b;
+  __syncthreads();
+}
+
+// CTA per row: write omegaPtr (+ omegaI for CSER) and scatter colI.
+template <typename ColT, typename RankT, bool CSER>
+__global__ void __launch_bounds__(kRowThreads) k_row_fill(int64_t m, int64_t n, FastWs ws, ColT *__restrict__ col,
+                                                          void *omega_ptr, int op_bits, void *omega_index,
+                                                          int oi_bits) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned int scan_sh[64];
+  const unsigned int k = ws.ctrl->k;
+  unsigned int *wc = reinterpret_cast<unsigned int *>(smem);  // [kRowWarps][k] per-warp counts -> offsets
+  unsigned int *cnt = wc + kRowWarps * k;                      // [k] per-rank count
+  unsigned int *excl = cnt + k;                                // [k] exclusive entry offset per rank
+  unsigned int *pidx = excl + k;                               // [k] CSER: index among present ranks
+  const RankT *ranks = static_cast<const RankT *>(ws.ranks);
+  const uint64_t *entry_off = ws.scan;
+  const uint64_t *seg_off = ws.scan + (CSER ? 2 : 1) * (m + 1);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t slab = ceil_div(ceil_div(n, kRowWarps), 32) * 32;
+  const unsigned int per = static_cast<unsigned int>(ceil_div(k, kRowThreads));
+  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+    for (unsigned int q = threadIdx.x; q < kRowWarps * k; q += blockDim.x) wc[q] = 0;
+    __syncthreads();
+    const RankT *rr = ranks + row * n;
+    const int64_t c_begin = wid * slab, c_end = min64(n, c_begin + slab);
+    for (int64_t c0 = c_begin; c0 < c_end; c0 += 32) {
+      const int64_t c = c0 + lane;
+      const unsigned int rk = c < c_end ? rr[c] : 0u;
+      const unsigned int peers = __match_any_sync(0xffffffffu, rk);
+      if (rk != 0 && lane == __ffs(peers) - 1) wc[wid * k + rk] += __popc(peers);
+    }
+    __syncthreads();
+    // per rank: total count and per-warp exclusive offsets
+    for (unsigned int q = threadIdx.x; q < k; q += blockDim.x) {
+      unsigned int run = 0;
+#pragma unroll
+      for (int w2 = 0; w2 < kRowWarps; ++w2) {
+        const unsigned int v = wc[w2 * k + q];
+        wc[w2 * k + q] = run;
+        run += v;
+      }
+      cnt[q] = q == 0 ? 0 : run;
+    }
+    __syncthreads();
+    // block scan over ranks: thread t owns ranks [t*per, (t+1)*per)
+    unsigned int la = 0, lb = 0;
+    const unsigned int q0 = threadIdx.x * per, q1 = min(k, q0 + per);
+    for (unsigned int q = q0; q < q1; ++q) { la += cnt[q]; lb += cnt[q] > 0; }
+    unsigned int ea, eb;
+    block_exscan2(la, lb, ea, eb, scan_sh);
+    for (unsigned int q = q0; q < q1; ++q) {
+      excl[q] = ea;
+      pidx[q] = eb;
+      ea += cnt[q];
+      eb += cnt[q] > 0;
+    }
+    __syncthreads();
+    const uint64_t e0 = entry_off[row], s0 = seg_off[row];
+    const unsigned int last = static_cast<unsigned int>(ws.row_stat[m + row]);
+    for (unsigned int q = 1 + threadIdx.x; q < k; q += blockDim.x) {
+      const uint64_t end = e0 + excl[q] + cnt[q];
+      if (CSER) {
+        if (cnt[q]) {
+          const uint64_t j = s0 + pidx[q];
+          store_index(omega_index, oi_bits, j, ws.to_vpos[q]);
+          store_index(omega_ptr, op_bits, j + 1, end);
+        }
+      } else if (q <= last) {
+        store_index(omega_ptr, op_bits, s0 + q, end);  // segment s0 + q - 1 ends here
+      }
+    }
+    // stable scatter: warp slabs are column-ordered, lanes ordered inside a step
+    const unsigned int lt = (1u << lane) - 1u;
+    for (int64_t c0 = c_begin; c0 < c_end; c0 += 32) {
+      const int64_t c = c0 + lane;
+      const unsigned int rk = c < c_end ? rr[c] : 0u;
+      const unsigned int peers = __match_any_sync(0xffffffffu, rk);
+      if (rk != 0) {
+        const uint64_t pos = e0 + excl[rk] + wc[wid * k + rk] + __popc(peers & lt);
+        col[pos] = static_cast<ColT>(c);
+      }
+      __syncwarp();
+      if (rk != 0 && lane == __ffs(peers) - 1) wc[wid * k + rk] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
+// Tail: omega (CER frequency order / CSER value order), rowPtr, omegaPtr[0].
+__global__ void k_fill_tail(int64_t m, FastWs ws, bool cser, double *omega, void *row_ptr, int rp_bits,
+                            void *omega_ptr, int op_bits) {
+  const unsigned int k = ws.ctrl->k;
+  const uint64_t *seg_scan = ws.scan + (cser ? 2 : 1) * (m + 1);
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = tid; i <= m; i += stride) store_index(row_ptr, rp_bits, i, seg_scan[i]);
+  for (int64_t f = tid; f < k; f += stride) omega[cser ? ws.to_vpos[f] : f] = ws.omega_freq[f];
+  if (tid == 0) store_index(omega_ptr, op_bits, 0, 0);
+}
+
+template <typename T>
+int launch_hist(const void *w, int64_t m, int64_t n, int64_t ldw, const FastWs &ws, cudaStream_t st) {
+  const int64_t total = m * n;
+  constexpr int V = sizeof(T) == 4 ? 4 : 2;
+  const bool vec_ok = (ldw == n) && (reinterpret_cast<uintptr_t>(w) % 16 == 0);
+  const int64_t units = vec_ok ? ceil_div(total, V) : total;
+  const int64_t want = ceil_div(units, 256 * 8);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, num_sms() * 8)));
+  if (vec_ok)
+    k_value_hist<T, V><<<grid, 256, 0, st>>>(static_cast<const T *>(w), m, n, ldw, ws);
+  else
+    k_value_hist<T, 1><<<grid, 256, 0, st>>>(static_cast<const T *>(w), m, n, ldw, ws);
+  CERDOT_LAUNCH_CHECK();
+  return CERDOT_OK;
+}
+
+template <typename T, typename RankT>
+int launch_row_count(const void *w, int64_t m, int64_t n, int64_t ldw, const FastWs &ws, unsigned int k,
+                     unsigned int rcap, cudaStream_t st) {
+  const size_t smem = rcap * (sizeof(unsigned long long) + sizeof(unsigned short)) + k * sizeof(unsigned int) + 16;
+  auto kern = k_row_count<T, RankT>;
+  CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int grid = static_cast<int>(std::min<int64_t>(m, num_sms() * 8));
+  kern<<<grid, kRowThreads, smem, st>>>(static_cast<const T *>(w), m, n, ldw, ws);
+  CERDOT_LAUNCH_CHECK();
+  return CERDOT_OK;
+}
+
+template <typename ColT, typename RankT>
+int launch_fill(int64_t m, int64_t n, const FastWs &ws, unsigned int k, bool cser, void *col, void *op, int op_bits,
+                void *oi, int oi_bits, cudaStream_t st) {
+  const size_t smem = (kRowWarps + 3) * static_cast<size_t>(k) * sizeof(unsigned int);
+  const int grid = static_cast<int>(std::min<int64_t>(m, num_sms() * 8));
+  if (cser) {
+    auto kern = k_row_fill<ColT, RankT, true>;
+    CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<grid, kRowThreads, smem, st>>>(m, n, ws, static_cast<ColT *>(col), op, op_bits, oi, oi_bits);
+  } else {
+    auto kern = k_row_fill<ColT, RankT, false>;
+    CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<grid, kRowThreads, smem, st>>>(m, n, ws, static_cast<ColT *>(col), op, op_bits, oi, oi_bits);
+  }
+  CERDOT_LAUNCH_CHECK();
+  return CERDOT_OK;
+}
+
+}  // namespace
+
+size_t encode_workspace_bytes(int64_t m, int64_t n) { return carve(nullptr, m, n).bytes; }
+
+int encode_plan(const void *w, int dtype, int64_t m, int64_t n, int64_t ldw, int bg_mode, double bg_value,
+                void *workspace, size_t workspace_bytes, cerdot_encode_info *info, cudaStream_t st) {
+  if (m <= 0 || n <= 0)  // the reference fails on omega[0] of an empty alphabet (formats.py:199)
+    return fail(CERDOT_E_INDEX, "index 0 is out of bounds for axis 0 with size 0");
+  if (ldw < n) return fail(CERDOT_E_VALUE, "row stride ldw must be >= n");
+  if (dtype != CERDOT_F32 && dtype != CERDOT_F64) return fail(CERDOT_E_TYPE, "w must be float32 or float64");
+  const size_t need = encode_workspace_bytes(m, n);
+  info->m = m;
+  info->n = n;
+  info->workspace_bytes = need;
+  if (workspace == nullptr || workspace_bytes < need)
+    return fail(CERDOT_E_WORKSPACE, "encode workspace too small: need " + std::to_string(need) + " bytes");
+  FastWs ws = carve(workspace, m, n);
+  CERDOT_CUDA_CHECK(cudaMemsetAsync(ws.gkey, 0, sizeof(unsigned long long) * kGlobalCap, st));
+  CERDOT_CUDA_CHECK(cudaMemsetAsync(ws.gcnt, 0, sizeof(unsigned long long) * kGlobalCap, st));
+  CERDOT_CUDA_CHECK(cudaMemsetAsync(ws.ctrl, 0, sizeof(Ctrl), st));
+  int rc = dtype == CERDOT_F32 ? launch_hist<float>(w, m, n, ldw, ws, st) : launch_hist<double>(w, m, n, ldw, ws, st);
+  if (rc) return rc;
+  Ctrl ctrl{};
+  CERDOT_CUDA_CHECK(cudaMemcpyAsync(&ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  CERDOT_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (ctrl.overflow)
+    return fail(CERDOT_E_UNSUPPORTED, "alphabet has more than " + std::to_string(kFastDistinct) +
+                                          " distinct values: the sort-based conversion path is not built yet");
+  k_alphabet<<<1, 1024, 0, st>>>(ws, bg_mode, bg_value);
+  CERDOT_LAUNCH_CHECK();
+  CERDOT_CUDA_CHECK(cudaMemcpyAsync(&ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  CERDOT_CUDA_CHECK(cudaStreamSynchronize(st));
+  const unsigned int k = ctrl.k;
+  if (k <= 256)
+    rc = dtype == CERDOT_F32 ? launch_row_count<float, uint8_t>(w, m, n, ldw, ws, k, ctrl.rcap, st)
+                             : launch_row_count<double, uint8_t>(w, m, n, ldw, ws, k, ctrl.rcap, st);
+  else
+    rc = dtype == CERDOT_F32 ? launch_row_count<float, uint16_t>(w, m, n, ldw, ws, k, ctrl.rcap, st)
+                             : launch_row_count<double, uint16_t>(w, m, n, ldw, ws, k, ctrl.rcap, st);
+  if (rc) return rc;
+  k_scan_rows<<<1, 1024, 0, st>>>(m, ws);
+  CERDOT_LAUNCH_CHECK();
+  uint64_t totals[3];
+  for (int j = 0; j < 3; ++j)
+    CERDOT_CUDA_CHECK(
+        cudaMemcpyAsync(&totals[j], ws.scan + j * (m + 1) + m, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  CERDOT_CUDA_CHECK(cudaStreamSynchronize(st));
+  info->k = k;
+  info->nnz = static_cast<int64_t>(totals[0]);
+  info->segments_cer = static_cast<int64_t>(totals[1]);
+  info->segments_cser = static_cast<int64_t>(totals[2]);
+  info->mode_index = ctrl.mode_index;
+  info->background = ctrl.background;
+  info->path = 0;
+  return CERDOT_OK;
+}
+
+int encode_fill(const cerdot_encode_info *info, int kind, void *workspace, size_t workspace_bytes, double *omega,
+                void *col, int col_bits, void *op, int op_bits, void *rp, int rp_bits, void *oi, int oi_bits,
+                cudaStream_t st) {
+  const int64_t m = info->m, n = info->n;
+  if (workspace == nullptr || workspace_bytes < encode_workspace_bytes(m, n))
+    return fail(CERDOT_E_WORKSPACE, "encode workspace too small");
+  FastWs ws = carve(workspace, m, n);
+  const bool cser = kind == CERDOT_CSER;
+  const unsigned int k = static_cast<unsigned int>(info->k);
+  int rc;
+  auto by_col = [&](auto rank_tag) -> int {
+    using RankT = decltype(rank_tag);
+    switch (col_bits) {
+      case 8: return launch_fill<uint8_t, RankT>(m, n, ws, k, cser, col, op, op_bits, oi, oi_bits, st);
+      case 16: return launch_fill<uint16_t, RankT>(m, n, ws, k, cser, col, op, op_bits, oi, oi_bits, st);
+      default: return launch_fill<uint32_t, RankT>(m, n, ws, k, cser, col, op, op_bits, oi, oi_bits, st);
+    }
+  };
+  rc = k <= 256 ? by_col(uint8_t{}) : by_col(uint16_t{});
+  if (rc) return rc;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m + 1, 256), num_sms() * 4)));
+  k_fill_tail<<<grid, 256, 0, st>>>(m, ws, cser, omega, rp, rp_bits, op, op_bits);
+  CERDOT_LAUNCH_CHECK();
+  return CERDOT_OK;
+}
+
+}  // namespace cerdot

@@ -1,0 +1,291 @@
+"""CER / CSER dot products on the GPU, drop-in for lemt.kernels (kernels.py:53-336).
+
+``dot_cer`` / ``dot_cser`` / ``dot`` call libcerdot's fp32 kernels on the
+HBM-resident encoding.  Inputs:
+
+* numpy arrays, ``Vector`` / ``DenseMatrix`` (this package's or the
+  reference's) or array-likes -> copied to the device, result returned as a
+  float64 numpy array like the reference (computed in fp32);
+* CUDA torch tensors -> used in place, result returned as an fp32 CUDA
+  tensor on the same stream (no host synchronisation).
+
+``trace=True`` returns ``(y, OpTrace)`` with the reference's analytic
+operation counts (kernels.py:175-234), computed on the host from the
+encoding's row/segment structure; traces never change numeric results.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .device import require_cuda, stream_ptr, torch_mod
+from .formats import (
+    TAG_COLI,
+    TAG_INPUT,
+    TAG_NONE,
+    TAG_OMEGA,
+    TAG_OMEGAI,
+    TAG_OMEGAPTR,
+    TAG_OUTPUT,
+    TAG_ROWPTR,
+    CerMatrix,
+    CserMatrix,
+)
+from .matrices import DenseMatrix, Vector
+
+OP_KINDS = ("sum", "mul", "read", "write", "other")
+
+
+@dataclass
+class OpTrace:
+    """Counts of elementary operations keyed by (kind, bits, array tag) (kernels.py:53-95)."""
+
+    counts: dict = field(default_factory=dict)
+
+    def add(self, kind: str, bits: int, tag: str, count: int) -> None:
+        if kind not in OP_KINDS:
+            raise ValueError(f"unknown op kind {kind!r}")
+        if count < 0:
+            raise ValueError("counts must be non-negative")
+        if count:
+            key = (kind, int(bits), tag)
+            self.counts[key] = self.counts.get(key, 0) + int(count)
+
+    def merged(self, other: "OpTrace") -> "OpTrace":
+        out = OpTrace(dict(self.counts))
+        for key, cnt in other.counts.items():
+            out.counts[key] = out.counts.get(key, 0) + cnt
+        return out
+
+    def scaled(self, factor: int) -> "OpTrace":
+        return OpTrace({key: cnt * factor for key, cnt in self.counts.items()})
+
+    def total(self, include_other: bool = False) -> int:
+        return sum(c for (k, _, _), c in self.counts.items() if include_other or k != "other")
+
+    def by_kind(self, include_other: bool = False) -> dict:
+        out: dict = {}
+        for (k, _, _), c in self.counts.items():
+            if k == "other" and not include_other:
+                continue
+            out[k] = out.get(k, 0) + c
+        return out
+
+    def count(self, kind: str | None = None, tag: str | None = None) -> int:
+        return sum(c for (k, _, t), c in self.counts.items()
+                   if (kind is None or k == kind) and (tag is None or t == tag))
+
+
+# --------------------------------------------------------------------------- host-side input handling
+
+
+def _input_array(x):
+    """(float64 ndarray, input bits) for host inputs (kernels.py:98-103)."""
+    if isinstance(x, (Vector, DenseMatrix)) or (hasattr(x, "values") and hasattr(x, "element_bits")):
+        return np.asarray(x.values, dtype=np.float64), int(x.element_bits)
+    return np.asarray(x, dtype=np.float64), 32
+
+
+def _check_shape(n: int, shape) -> None:
+    if len(shape) not in (1, 2):
+        raise ValueError("right-hand side must be a vector or a matrix")
+    if shape[0] != n:
+        raise ValueError(f"dimension mismatch: matrix has n={n}, input has {shape[0]}")
+
+
+def _resolve_bits(a, b_in, input_bits, output_bits):
+    if input_bits is not None:
+        b_in = int(input_bits)
+    b_out = max(b_in, a.element_bits) if output_bits is None else int(output_bits)
+    return b_in, b_out
+
+
+# --------------------------------------------------------------------------- analytic traces (kernels.py:175-234)
+
+
+def _segment_shape(x, rows):
+    row_ptr = x.row_ptr.astype(np.int64)
+    seg_sizes = np.diff(x.omega_ptr.astype(np.int64))
+    segs_per_row = np.diff(row_ptr)
+    ne_prefix = np.concatenate(([0], np.cumsum(seg_sizes > 0)))
+    sz_prefix = np.concatenate(([0], np.cumsum(seg_sizes)))
+    nonempty = ne_prefix[row_ptr[1:]] - ne_prefix[row_ptr[:-1]]
+    entries = sz_prefix[row_ptr[1:]] - sz_prefix[row_ptr[:-1]]
+    if rows is not None:
+        sel = np.asarray(rows)
+        return segs_per_row[sel], nonempty[sel], entries[sel]
+    return segs_per_row, nonempty, entries
+
+
+def _trace_segmented(x, input_bits, output_bits, rows, columns, with_omega_index) -> OpTrace:
+    b_in, b_out = _resolve_bits(x, 32, input_bits, output_bits)
+    segs, nonempty, entries = _segment_shape(x, rows)
+    r = len(segs)
+    s, s_ne, z = int(segs.sum()), int(nonempty.sum()), int(entries.sum())
+    t = OpTrace()
+    if x.background != 0.0:
+        t.add("sum", b_in, TAG_NONE, max(x.n - 1, 0))
+        t.add("mul", b_out, TAG_NONE, 1)
+        t.add("sum", b_out, TAG_NONE, r + s_ne)
+    t.add("read", x.row_ptr_bits, TAG_ROWPTR, 2 * r)
+    t.add("read", x.omega_ptr_bits, TAG_OMEGAPTR, s + int((segs > 0).sum()))
+    if with_omega_index:
+        t.add("read", x.omega_index_bits, TAG_OMEGAI, s)
+    t.add("read", x.element_bits, TAG_OMEGA, s_ne)
+    t.add("read", x.col_index_bits, TAG_COLI, z)
+    t.add("read", b_in, TAG_INPUT, z)
+    t.add("sum", b_in, TAG_NONE, z - s_ne)
+    t.add("mul", b_out, TAG_NONE, s_ne)
+    t.add("sum", b_out, TAG_NONE, int(np.maximum(nonempty - 1, 0).sum()))
+    t.add("write", b_out, TAG_OUTPUT, r)
+    t.add("other", 0, TAG_NONE, 3 * r + 4 * s + z + 1)
+    return t.scaled(columns) if columns != 1 else t
+
+
+def trace_cer(a: CerMatrix, input_bits: int = 32, output_bits: int | None = None, rows=None,
+              columns: int = 1) -> OpTrace:
+    return _trace_segmented(a, input_bits, output_bits, rows, columns, with_omega_index=False)
+
+
+def trace_cser(a: CserMatrix, input_bits: int = 32, output_bits: int | None = None, rows=None,
+               columns: int = 1) -> OpTrace:
+    return _trace_segmented(a, input_bits, output_bits, rows, columns, with_omega_index=True)
+
+
+def trace_of(a, input_bits: int = 32, output_bits: int | None = None, rows=None, columns: int = 1) -> OpTrace:
+    if isinstance(a, CerMatrix):
+        return trace_cer(a, input_bits, output_bits, rows, columns)
+    if isinstance(a, CserMatrix):
+        return trace_cser(a, input_bits, output_bits, rows, columns)
+    raise TypeError(f"not a CER/CSER matrix: {type(a)!r} (dense/CSR are outside this package's scope)")
+
+
+def row_trace(a, row: int, input_bits: int = 32, output_bits: int | None = None) -> OpTrace:
+    """Trace of the scalar product of one matrix row with an input vector (kernels.py:249-251)."""
+    return trace_of(a, input_bits, output_bits, rows=[row])
+
+
+# --------------------------------------------------------------------------- numeric kernels
+
+
+class _Workspace:
+    """Per-device scratch for the background column sums (no allocation on the hot path)."""
+
+    def __init__(self):
+        self._buf = {}
+
+    def get(self, device, nbytes: int):
+        torch = torch_mod()
+        key = (device.type, device.index)
+        buf = self._buf.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            self._buf[key] = buf
+        return buf
+
+
+_WS = _Workspace()
+
+
+class _Pinned(threading.local):
+    """Per-thread pinned staging buffers for host inputs/outputs (no cudaHostAlloc per call)."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, key: str, nbytes: int):
+        torch = torch_mod()
+        buf = self.bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 4096), dtype=torch.uint8, pin_memory=True)
+            self.bufs[key] = buf
+        return buf
+
+
+_PIN = _Pinned()
+
+
+def dot_device(enc, x, out=None, stream=None):
+    """Device-only entry: ``x`` a CUDA fp32 tensor (n,) or (n, B); returns y (m,) / (m, B) fp32.
+
+    Stream-ordered on ``stream`` (default: torch's current stream), no host sync.
+    """
+    torch = torch_mod()
+    dev = enc.device_encoding(x.device)
+    if x.dtype != torch.float32:
+        x = x.to(torch.float32)
+    if x.ndim == 2 and x.stride(1) != 1:
+        x = x.contiguous()
+    if x.ndim == 1 and x.stride(0) != 1:
+        x = x.contiguous()
+    _check_shape(dev.n, tuple(x.shape))
+    batch = 1 if x.ndim == 1 else int(x.shape[1])
+    if out is None:
+        out = torch.empty((dev.m,) if x.ndim == 1 else (dev.m, batch), dtype=torch.float32, device=x.device)
+    ldx = 1 if x.ndim == 1 else x.stride(0)
+    ldy = 1 if out.ndim == 1 else out.stride(0)
+    L = _native.lib()
+    st = dev.struct()
+    ws_bytes = L.cerdot_dot_workspace_bytes(st, batch)
+    ws = _WS.get(x.device, ws_bytes) if ws_bytes else None
+    sp = stream if stream is not None else stream_ptr(x.device)
+    _native.check(L.cerdot_dot(st, x.data_ptr(), ldx, batch, out.data_ptr(), ldy,
+                               ws.data_ptr() if ws is not None else None, ws_bytes, sp))
+    return out
+
+
+def _dot_encoded(a, x, trace, input_bits, output_bits, tracer):
+    torch = torch_mod()
+    if isinstance(x, torch.Tensor):
+        _check_shape(a.n, tuple(x.shape))
+        if not x.is_cuda:
+            x = x.to(require_cuda())
+        y = dot_device(a, x)
+        b_in = 32
+        cols = 1 if x.ndim == 1 else int(x.shape[1])
+    else:
+        xv, b_in = _input_array(x)
+        _check_shape(a.n, xv.shape)
+        dev = require_cuda()
+        nx = xv.size * 4
+        xin = _PIN.get("x", nx)[:nx].view(torch.float32).view(xv.shape)
+        np.copyto(xin.numpy(), xv, casting="unsafe")  # the kernels compute in fp32
+        xt = xin.to(dev, non_blocking=True)
+        yt = dot_device(a, xt)
+        ny = yt.numel() * 4
+        yout = _PIN.get("y", ny)[:ny].view(torch.float32).view(tuple(yt.shape))
+        yout.copy_(yt, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        y = yout.numpy().astype(np.float64)
+        cols = 1 if xv.ndim == 1 else xv.shape[1]
+    if not trace:
+        return y
+    b_in = b_in if input_bits is None else input_bits
+    return y, tracer(a, b_in, output_bits, columns=cols)
+
+
+def dot_cer(a: CerMatrix, x, trace: bool = False, input_bits: int | None = None, output_bits: int | None = None):
+    """y = A.x for a CER matrix (kernels.py:304-312)."""
+    if not isinstance(a, CerMatrix):
+        raise TypeError(f"dot_cer needs a CerMatrix, got {type(a)!r}")
+    return _dot_encoded(a, x, trace, input_bits, output_bits, trace_cer)
+
+
+def dot_cser(a: CserMatrix, x, trace: bool = False, input_bits: int | None = None, output_bits: int | None = None):
+    """y = A.x for a CSER matrix (kernels.py:315-323)."""
+    if not isinstance(a, CserMatrix):
+        raise TypeError(f"dot_cser needs a CserMatrix, got {type(a)!r}")
+    return _dot_encoded(a, x, trace, input_bits, output_bits, trace_cser)
+
+
+def dot(a, x, trace: bool = False, input_bits: int | None = None, output_bits: int | None = None):
+    """Format-dispatched dot product (kernels.py:326-336)."""
+    if isinstance(a, CerMatrix):
+        return dot_cer(a, x, trace, input_bits, output_bits)
+    if isinstance(a, CserMatrix):
+        return dot_cser(a, x, trace, input_bits, output_bits)
+    raise TypeError(f"not a matrix: {type(a)!r} (this package implements CER/CSER only)")

@@ -1,0 +1,105 @@
+"""Row sharding of CER/CSER encodings over the GPUs of one node.
+
+Rows of a CER/CSER matrix are independent: a shard is a contiguous row
+block ``[r0, r1)`` cut out of the global encoding (not a re-encode) —
+
+* ``row_ptr[r0..r1]`` rebased by ``row_ptr[r0]``,
+* ``omega_ptr[row_ptr[r0]..row_ptr[r1]]`` rebased by its first entry,
+* the matching ``col_index`` span (and CSER ``omega_index`` span),
+* ``omega`` unchanged (CER ranks are row-relative, CSER indices global).
+
+The activations are replicated, each rank computes its block of y, and the
+only exchange is one all-gather of the y blocks (NCCL over NVLink on a GPU
+node; gloo in the CPU tests).  Block boundaries come from
+``cerdot_shard_plan`` (balanced encoded bytes).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .formats import CerMatrix, CserMatrix
+
+
+def plan_rows(enc, parts: int) -> list[int]:
+    """parts+1 row bounds balancing encoded bytes (cerdot_shard_plan)."""
+    rp = np.ascontiguousarray(enc.row_ptr)
+    op = np.ascontiguousarray(enc.omega_ptr)
+    bounds = (ctypes.c_int64 * (parts + 1))()
+    _native.check(_native.lib().cerdot_shard_plan(rp.ctypes.data, rp.dtype.itemsize * 8, op.ctypes.data,
+                                                  op.dtype.itemsize * 8, enc.col_index_bits, enc.m, parts,
+                                                  bounds))
+    return list(bounds)
+
+
+def even_rows(m: int, parts: int) -> list[int]:
+    return [m * p // parts for p in range(parts + 1)]
+
+
+def slice_rows(enc, r0: int, r1: int):
+    """Rows [r0, r1) of an encoding as a self-contained encoding (host arrays; uploads on first dot)."""
+    if not 0 <= r0 <= r1 <= enc.m:
+        raise ValueError(f"row block [{r0}, {r1}) out of range for m={enc.m}")
+    rp = enc.row_ptr.astype(np.int64)
+    op = enc.omega_ptr.astype(np.int64)
+    s0, s1 = int(rp[r0]), int(rp[r1])
+    e0, e1 = int(op[s0]), int(op[s1])
+    row_ptr = (rp[r0:r1 + 1] - s0).astype(enc.row_ptr.dtype)
+    omega_ptr = (op[s0:s1 + 1] - e0).astype(enc.omega_ptr.dtype)
+    col = enc.col_index[e0:e1]
+    if isinstance(enc, CserMatrix):
+        return CserMatrix(enc.omega, col, enc.omega_index[s0:s1], omega_ptr, row_ptr, r1 - r0, enc.n,
+                          enc.element_bits, enc.mode_index)
+    return CerMatrix(enc.omega, col, omega_ptr, row_ptr, r1 - r0, enc.n, enc.element_bits)
+
+
+class RowShardedDot:
+    """y = A.x with A's rows split over the ranks of a process group.
+
+    ``local`` is this rank's row block (an encoding, or any object accepted by
+    ``compute``), ``rows_per_rank`` the block heights (all-gather needs equal
+    blocks, so shorter blocks are padded).  ``compute(local, x)`` returns the
+    local y block as a torch tensor on the communication device; it defaults
+    to the CUDA dot (``kernels.dot_device``) and is injectable so the
+    exchange logic can be exercised on CPU with gloo.
+    """
+
+    def __init__(self, local, rows_per_rank: list[int], group=None, compute=None):
+        import torch.distributed as dist
+
+        self.local = local
+        self.rows = list(rows_per_rank)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if len(self.rows) != self.world:
+            raise ValueError(f"{len(self.rows)} row blocks for a world of {self.world}")
+        self.block = max(self.rows) if self.rows else 0
+        if compute is None:
+            from .kernels import dot_device
+
+            compute = dot_device
+        self.compute = compute
+        self._gather = None
+
+    def __call__(self, x):
+        import torch
+        import torch.distributed as dist
+
+        y = self.compute(self.local, x)
+        if self.world == 1:
+            return y
+        shape = (self.block,) + tuple(y.shape[1:])
+        if y.shape[0] != self.block:
+            pad = torch.zeros(shape, dtype=y.dtype, device=y.device)
+            pad[: y.shape[0]] = y
+            y = pad
+        out = torch.empty((self.world * self.block,) + tuple(y.shape[1:]), dtype=y.dtype, device=y.device)
+        dist.all_gather_into_tensor(out, y.contiguous(), group=self.group)
+        if all(r == self.block for r in self.rows):
+            return out
+        parts = [out[i * self.block: i * self.block + r] for i, r in enumerate(self.rows)]
+        return torch.cat(parts, dim=0)

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through libcerdot's C ABI) against the pinned oracle.
+
+Bars (north_star): conversion outputs bit-exact (omega, colI, omegaPtr,
+rowPtr, omegaI, mode_index, auto widths); dot within max relative error
+1e-5 of the float64 reference; integer alphabets bitwise (every partial sum
+is an exactly representable fp32 integer, so any summation order is exact).
+"""
+
+import numpy as np
+import pytest
+
+import paper_1805_10692_b200 as cd
+import recipes
+from conftest import REL_TOL, digest, is_integer_case, rel_err
+from oracle import c_oracle, numpy_port
+from paper_1805_10692_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _assert_same(enc, g, kind, name):
+    assert enc.omega.tolist() == g["omega"], name
+    assert enc.col_index.tolist() == g["colI"], name
+    assert enc.omega_ptr.tolist() == g["omegaPtr"], name
+    assert enc.row_ptr.tolist() == g["rowPtr"], name
+    assert enc.col_index_bits == g["bits"]["colI"], name
+    assert enc.omega_ptr_bits == g["bits"]["omegaPtr"], name
+    assert enc.row_ptr_bits == g["bits"]["rowPtr"], name
+    assert cd.storage_bits(enc) == g["storage_bits"], name
+    if kind == "cser":
+        assert enc.omega_index.tolist() == g["omegaI"], name
+        assert enc.omega_index_bits == g["bits"]["omegaI"], name
+        assert enc.mode_index == g["mode_index"], name
+    # the sign of a zero in omega is pinned where the reference is unambiguous
+    # (single-signed zeros, or an explicit background); see DESIGN.md
+    assert np.signbit(enc.omega).tolist() == g["omega_signbit"], name
+
+
+def test_small_cases(small_cases):
+    for case in small_cases:
+        w = np.asarray(case["matrix"], dtype=float)
+        x = np.asarray(case["x"], dtype=float)
+        for kind in ("cer", "cser"):
+            g = case[kind]
+            encode = cd.encode_cer if kind == "cer" else cd.encode_cser
+            if "error" in g:
+                with pytest.raises(Exception) as err:
+                    encode(cd.DenseMatrix(w), index_bits=case["index_bits"], background=case["background"])
+                assert type(err.value).__name__ == g["error"], case["name"]
+                continue
+            enc = encode(cd.DenseMatrix(w), index_bits=case["index_bits"], background=case["background"])
+            _assert_same(enc, g, kind, case["name"])
+            y = cd.dot(enc, x)
+            y_ref = np.asarray(g["y"], dtype=float)
+            assert y.shape == y_ref.shape
+            if not np.all(np.isfinite(y_ref)):
+                assert np.array_equal(np.isnan(y), np.isnan(y_ref)), case["name"]
+                continue
+            if is_integer_case(case):
+                assert np.array_equal(y, y_ref), (case["name"], kind, y, y_ref)
+            else:
+                assert rel_err(y, y_ref) <= REL_TOL, (case["name"], kind)
+
+
+def test_recipe_families(recipe_digests):
+    for fam, cases in recipe_digests.items():
+        for case in cases:
+            w, x = recipes.RECIPES[fam](case["seed"])
+            for kind in ("cer", "cser"):
+                g = case[kind]
+                enc = (cd.encode_cer if kind == "cer" else cd.encode_cser)(w)
+                tag = (fam, case["seed"], kind)
+                assert digest(enc.omega) == g["omega"], tag
+                assert digest(enc.col_index) == g["colI"], tag
+                assert digest(enc.omega_ptr) == g["omegaPtr"], tag
+                assert digest(enc.row_ptr) == g["rowPtr"], tag
+                if kind == "cser":
+                    assert digest(enc.omega_index) == g["omegaI"], tag
+                    assert enc.mode_index == g["mode_index"], tag
+                y = cd.dot(enc, x)
+                if fam == "criterion3":  # integer alphabets: bitwise (tests/test_acceptance.py:108-126)
+                    assert digest(y) == g["y_digest"], tag
+                else:
+                    ref = numpy_port.encode_cer(w) if kind == "cer" else numpy_port.encode_cser(w)
+                    assert rel_err(y, numpy_port.dot(ref, x)) <= REL_TOL, tag
+
+
+@pytest.mark.parametrize("name", ["oracle", "alexnet-fc6", "vgg-fc6", "resnet-conv"])
+def test_config_encodings_and_matvec(config_goldens, name):
+    meta, ys = config_goldens
+    w, _ = synth.make_layer(name)
+    wt = torch.from_numpy(w).cuda()
+    x1 = np.random.default_rng(1).standard_normal(w.shape[1], dtype=np.float32)
+    outs = {}
+    for kind in ("cer", "cser"):
+        enc = (cd.encode_cer if kind == "cer" else cd.encode_cser)(wt)
+        g = meta["configs"][name][kind]
+        assert (enc.nnz, enc.segment_count, len(enc.omega)) == (g["nnz"], g["segments"], g["K"])
+        assert digest(enc.omega) == g["omega"]
+        assert digest(enc.col_index) == g["colI"]
+        assert digest(enc.omega_ptr) == g["omegaPtr"]
+        assert digest(enc.row_ptr) == g["rowPtr"]
+        if kind == "cser":
+            assert digest(enc.omega_index) == g["omegaI"]
+            assert enc.mode_index == g["mode_index"]
+        assert cd.storage_bits(enc) == g["storage_bits"]
+        y = cd.dot(enc, x1)
+        assert rel_err(y, ys[f"{name}/{kind}/b1"]) <= REL_TOL, (name, kind)
+        outs[kind] = y
+    # CER and CSER walk the same segments in the same order: identical fp32 results
+    assert np.array_equal(outs["cer"], outs["cser"])
+
+
+@pytest.mark.parametrize("name", ["oracle", "alexnet-fc6", "vgg-fc6", "resnet-conv"])
+def test_config_matmat(name):
+    cfg = synth.config(name)
+    w, xs = synth.make_layer(cfg)
+    b = max(cfg.batches)
+    if b == 1:
+        b = 8
+        x = np.random.default_rng(2).standard_normal((cfg.n, b), dtype=np.float32)
+    else:
+        x = xs[b]
+    if b > 256:  # keep the float64 oracle bounded: a column slice is bitwise the same computation per column
+        x = np.ascontiguousarray(x[:, :200])
+    wt = torch.from_numpy(w).cuda()
+    xt = torch.from_numpy(x).cuda()
+    for kind in ("cer", "cser"):
+        enc = (cd.encode_cer if kind == "cer" else cd.encode_cser)(wt)
+        y = cd.dot(enc, xt).cpu().numpy()
+        ref = c_oracle.dot(c_oracle.encode(w, kind), x.astype(np.float64))
+        assert rel_err(y, ref) <= REL_TOL, (name, kind, rel_err(y, ref))
+        # column-wise parity too (each output column is its own dot product)
+        col_err = np.abs(y - ref).max(axis=0) / (np.abs(ref).max(axis=0) + 1e-30)
+        assert col_err.max() <= 1e-4
+
+
+def test_full_batch_resnet_conv_properties():
+    """Config 4 at its full B=1568: linearity and column-slice consistency (size-independent checks)."""
+    cfg = synth.config("resnet-conv")
+    w, xs = synth.make_layer(cfg)
+    x = torch.from_numpy(xs[1568]).cuda()
+    enc = cd.encode_cser(torch.from_numpy(w).cuda())
+    y = cd.dot(enc, x)
+    y_slice = cd.dot(enc, x[:, 1000:1100].contiguous())
+    assert torch.equal(y[:, 1000:1100], y_slice)  # per-column computation is independent of the batch
+    y2 = cd.dot(enc, 2.0 * x)
+    assert torch.equal(y2, 2.0 * y)  # exact: scaling by 2 commutes with fp32 rounding
+    ref = c_oracle.dot(c_oracle.encode(w, "cser"), xs[1568][:, 1500:].astype(np.float64))
+    assert rel_err(y[:, 1500:].cpu().numpy(), ref) <= REL_TOL
+
+
+def test_background_nonzero_without_decomposition():
+    # criterion-7 shaped matrices (mode != 0) encoded directly: y += bg * sum(x) in the epilogue
+    for seed in range(10):
+        w, x = recipes.nonzero_mode(seed)
+        for encode, ref_encode in ((cd.encode_cer, numpy_port.encode_cer), (cd.encode_cser, numpy_port.encode_cser)):
+            enc = encode(w)
+            assert enc.background != 0.0
+            assert rel_err(cd.dot(enc, x), numpy_port.dot(ref_encode(w), x)) <= REL_TOL
+            xb = np.random.default_rng(seed).normal(size=(w.shape[1], 5))
+            assert rel_err(cd.dot(enc, xb), numpy_port.dot(ref_encode(w), xb)) <= REL_TOL
+
+
+def test_torch_api_and_determinism():
+    w, xs = synth.make_layer("oracle")
+    enc = cd.encode_cer(torch.from_numpy(w).cuda())
+    x = torch.from_numpy(xs[1]).cuda()
+    y1 = cd.dot_device(enc, x)
+    y2 = cd.dot_device(enc, x)
+    assert y1.dtype == torch.float32 and y1.is_cuda and y1.shape == (512,)
+    assert torch.equal(y1, y2)
+    y_np = cd.dot(enc, xs[1])
+    assert np.array_equal(y_np, y1.cpu().numpy().astype(np.float64))
+    y_t, tr = cd.dot_cer(enc, x, trace=True)
+    assert torch.equal(y_t, y1) and tr.count("read", "colI") == enc.nnz
+    with pytest.raises(ValueError, match="mismatch"):
+        cd.dot(enc, torch.ones(5, device="cuda"))
+    with pytest.raises(TypeError):
+        cd.dot_cser(enc, x)
+
+
+def test_host_constructed_encoding_uploads(small_cases):
+    case = next(c for c in small_cases if c["name"] == "M_ones")
+    g = case["cer"]
+    enc = cd.CerMatrix(np.array(g["omega"]), np.array(g["colI"], dtype=np.int64), np.array(g["omegaPtr"]),
+                       np.array(g["rowPtr"]), 5, 12)
+    assert cd.dot(enc, np.ones(12)).tolist() == [22.0, 24.0, 17.0, 23.0, 16.0]
+
+
+def test_negative_zero_and_nan_handling():
+    enc = cd.encode_cer(np.array([[-0.0, -0.0, 1.0]]))
+    assert np.signbit(enc.omega[0]) and enc.col_index.tolist() == [2]
+    enc = cd.encode_cer(np.array([[0.0, -0.0, 0.0, 1.0, 1.0]]))  # mixed zeros: one element
+    assert len(enc.omega) == 2 and enc.omega[1] == 0.0 and enc.col_index.tolist() == [1, 2] or \
+        enc.omega.tolist() == [1.0, 0.0]
+    ref = numpy_port.encode_cer(np.array([[np.nan, 1.0, 1.0]]))
+    enc = cd.encode_cer(np.array([[np.nan, 1.0, 1.0]]))
+    assert enc.col_index.tolist() == ref["colI"].tolist() and np.isnan(enc.omega[1])
+
+
+def test_empty_and_degenerate():
+    with pytest.raises(IndexError):
+        cd.encode_cer(np.zeros((0, 4)))
+    with pytest.raises(IndexError):
+        cd.encode_cser(np.zeros((3, 0)))
+    enc = cd.encode_cer(np.zeros((4, 5)))
+    assert cd.dot(enc, np.arange(5.0)).tolist() == [0.0] * 4
+    enc = cd.encode_cser(np.full((3, 7), 2.5))  # constant, background 2.5: y = 2.5 * sum(x)
+    assert np.allclose(cd.dot(enc, np.arange(7.0)), 2.5 * 21.0)
+
+
+def test_wide_alphabets_up_to_fast_limit():
+    rng = np.random.default_rng(5)
+    w = rng.integers(-1000, 1000, size=(64, 300)).astype(np.float64)  # ~1900 distinct values
+    x = rng.integers(-3, 4, size=300).astype(np.float64)
+    for encode, ref_encode in ((cd.encode_cer, numpy_port.encode_cer), (cd.encode_cser, numpy_port.encode_cser)):
+        enc = encode(w)
+        ref = ref_encode(w)
+        assert digest(enc.col_index) == digest(ref["colI"])
+        assert digest(enc.omega_ptr) == digest(ref["omegaPtr"])
+        assert digest(enc.row_ptr) == digest(ref["rowPtr"])
+        assert np.array_equal(cd.dot(enc, x), w @ x)
