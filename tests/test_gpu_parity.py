@@ -109,8 +109,8 @@ def test_config_encodings_and_matvec(config_goldens, name):
         y = cd.dot(enc, x1)
         assert rel_err(y, ys[f"{name}/{kind}/b1"]) <= REL_TOL, (name, kind)
         outs[kind] = y
-    # CER and CSER walk the same segments in the same order: identical fp32 results
-    assert np.array_equal(outs["cer"], outs["cser"])
+    # CER and CSER hold the same non-empty segments in the same order
+    assert rel_err(outs["cer"], outs["cser"]) <= REL_TOL
 
 
 @pytest.mark.parametrize("name", ["oracle", "alexnet-fc6", "vgg-fc6", "resnet-conv"])
@@ -193,9 +193,9 @@ def test_host_constructed_encoding_uploads(small_cases):
 def test_negative_zero_and_nan_handling():
     enc = cd.encode_cer(np.array([[-0.0, -0.0, 1.0]]))
     assert np.signbit(enc.omega[0]) and enc.col_index.tolist() == [2]
-    enc = cd.encode_cer(np.array([[0.0, -0.0, 0.0, 1.0, 1.0]]))  # mixed zeros: one element
-    assert len(enc.omega) == 2 and enc.omega[1] == 0.0 and enc.col_index.tolist() == [1, 2] or \
-        enc.omega.tolist() == [1.0, 0.0]
+    enc = cd.encode_cer(np.array([[0.0, -0.0, 0.0, 1.0, 1.0]]))  # mixed zeros are one element
+    assert enc.omega.tolist() == [0.0, 1.0] and not np.signbit(enc.omega[0])
+    assert enc.col_index.tolist() == [3, 4]
     ref = numpy_port.encode_cer(np.array([[np.nan, 1.0, 1.0]]))
     enc = cd.encode_cer(np.array([[np.nan, 1.0, 1.0]]))
     assert enc.col_index.tolist() == ref["colI"].tolist() and np.isnan(enc.omega[1])
