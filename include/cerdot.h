@@ -69,7 +69,8 @@ typedef struct {
   int64_t nnz;                /* len(col_index) */
   int64_t segments;           /* len(omega_ptr) - 1 */
   const double *omega;        /* (device) k: CER frequency-major, CSER value-ascending */
-  const void *col_index;      /* (device) nnz unsigned ints of col_bits */
+  const void *col_index;      /* (device) nnz unsigned ints of col_bits; readable up to the next
+                                 16-byte boundary past the last entry (vector loads) */
   const void *omega_ptr;      /* (device) segments+1 unsigned ints of omega_ptr_bits */
   const void *row_ptr;        /* (device) m+1 unsigned ints of row_ptr_bits */
   const void *omega_index;    /* (device) CSER: segments unsigned ints of omega_index_bits */

@@ -1,14 +1,35 @@
-// CER / CSER dot product on sm_100a, fp32.
+// CER / CSER dot product on sm_100a, fp32, no tensor cores.
 //
-// Reference: lemt kernels.py:283-301 (_dot_segmented) evaluated in float64:
-//   y[r] = sum_seg (omega[seg] - bg) * (sum_{i in seg} x[colI[i]])  (+ bg * sum(x) if bg != 0)
-// Summation order here (stated for the 1e-5 parity bar):
-//   * inner per-segment sums: sequential fp32 in colI order,
-//   * one fp32 fma per non-empty segment into a per-lane row accumulator,
-//   * lanes combined by a fixed xor-butterfly (deterministic),
-//   * background correction: sum(x) in fp64 (fixed tree), bg * sum in fp64,
-//     added to the fp32 row sum in fp64 and rounded once.
-// The segment value is (float)(omega[k] - bg) computed in fp64 per segment.
+// Reference: lemt kernels.py:283-301 (_dot_segmented), float64:
+//   y[r] = sum_seg (omega[seg] - bg) * (sum_{i in seg} x[colI[i]])  (+ bg * sum(x) when bg != 0)
+//
+// Mat-vec (batch 1) — k_matvec, HBM-bound:
+//   * persistent CTAs stage x in shared memory once (random gathers from smem
+//     cost ~3.5 bank-cycles per 32 lanes; from L1 they cost one wavefront per
+//     distinct 128 B line, ~9x more), plus the per-element segment values
+//     (float)(omega[k] - bg);
+//   * a warp walks one row in windows of 32 x EPL entries: every lane loads EPL
+//     consecutive colI entries with 16 B vector loads (coalesced stream), the
+//     next window is prefetched into registers;
+//   * the row's segment starts (omegaPtr) are registered lane-parallel into a
+//     per-warp slot table (slot = entry position -> element index k), so each
+//     lane knows where segments begin inside its run;
+//   * each lane sums its run segment by segment; a segment that ends inside the
+//     lane is multiplied there; pieces that cross lanes are joined by a warp
+//     segmented scan (fixed Hillis-Steele order) and multiplied once at the
+//     lane where the segment closes; the open segment carries across windows.
+//     Every non-empty segment is multiplied exactly once (kernels.py:296).
+// Mat-mat (batch > 1) — k_matmat, gather-bound (L2 -> SM):
+//   * a warp owns (row, 32*V batch columns); 32 entries at a time are loaded
+//     lane-parallel with their segment heads, then walked with V-wide vector
+//     loads of the X rows, eight in flight; one fma per segment per column.
+//
+// Summation order (the 1e-5 parity bar): fp32 segment sums
+// in colI order within a lane, lane pieces joined left-to-right by the scan;
+// one fp32 fma per segment into per-lane row accumulators; lanes combined by
+// an xor butterfly.  Background correction: sum(x) in fp64 (fixed tree),
+// bg*sum in fp64, added to the fp32 row sum in fp64, rounded once.
+// Deterministic: no floating-point atomics, fixed reduction order.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -22,6 +43,11 @@ namespace cerdot {
 
 namespace {
 
+constexpr int kMatvecThreads = 512;
+constexpr int kMatvecWarps = kMatvecThreads / 32;
+constexpr int kSmemValues = 4096;             // omega entries cached in smem
+constexpr int kMaxSmemBytes = 227 * 1024;
+
 struct DotArgs {
   const double *omega;
   const void *col;
@@ -29,7 +55,7 @@ struct DotArgs {
   const void *rp;
   const void *oi;
   int rp_bits, oi_bits;
-  int64_t m, n;
+  int64_t m, n, k;
   double bg;
   const double *colsum;  // batch doubles when bg != 0
 };
@@ -39,14 +65,307 @@ __device__ __forceinline__ uint32_t ld_idx(const T *p, int64_t i) {
   return __ldg(p + i);
 }
 
-__device__ __forceinline__ float seg_value(const DotArgs &a, bool cser, int64_t s, int64_t s0) {
-  const int64_t k = cser ? static_cast<int64_t>(load_index(a.oi, a.oi_bits, s)) : (s - s0 + 1);
-  return static_cast<float>(__ldg(a.omega + k) - a.bg);
+// 16-byte vector of indices -> unpacked u32 lanes
+template <typename ColT>
+struct ColVec;
+template <>
+struct ColVec<uint8_t> {
+  static constexpr int kPer = 16;
+  __device__ static void unpack(const uint4 &v, uint32_t *out) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) out[4 * i + b] = (w[i] >> (8 * b)) & 0xffu;
+  }
+};
+template <>
+struct ColVec<uint16_t> {
+  static constexpr int kPer = 8;
+  __device__ static void unpack(const uint4 &v, uint32_t *out) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      out[2 * i] = w[i] & 0xffffu;
+      out[2 * i + 1] = w[i] >> 16;
+    }
+  }
+};
+template <>
+struct ColVec<uint32_t> {
+  static constexpr int kPer = 4;
+  __device__ static void unpack(const uint4 &v, uint32_t *out) {
+    out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+  }
+};
+
+__device__ __forceinline__ uint4 ld_stream(const void *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
 }
 
-// Mat-vec: warp per row, lanes stride over the row's segments.
+// TMA-engine prefetch of a contiguous global range into L2 (no registers, no smem).
+__device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+constexpr int kEPL = 32;                      // entries per lane per window
+constexpr uint32_t kWin = 32 * kEPL;          // entries per window
+
+// Window-local prefix table of a warp: entry position p (lane p/32, item j=p%32) lives at
+// (j/4)*128 + lane*4 + j%4 so each lane writes its 32 prefixes as eight conflict-free 16 B stores.
+__device__ __forceinline__ uint32_t ppos(uint32_t p) { return ((p & 31u) >> 2) * 128u + (p >> 5) * 4u + (p & 3u); }
+
+// Gather x for one lane's 32 window entries (MASKED: only entries in [e0, e1)), build the lane's
+// running prefix sums and store them to the warp's prefix table; returns the lane total.
+template <typename ColT, bool XSMEM, bool MASKED>
+__device__ __forceinline__ float gather_prefix(const uint4 *raw_v, uint32_t w0, uint32_t e0, uint32_t e1,
+                                               const float *__restrict__ xs, const float *__restrict__ x, float *pre,
+                                               int lane) {
+  using CV = ColVec<ColT>;
+  constexpr int NV = kEPL / CV::kPer;
+  const uint32_t p0 = w0 + lane * kEPL;
+  uint32_t vmask = 0xffffffffu;
+  if (MASKED) {
+    const uint32_t jlo = e0 > p0 ? min(e0 - p0, 32u) : 0u;
+    const uint32_t jhi = e1 > p0 ? min(e1 - p0, 32u) : 0u;
+    vmask = (jhi >= 32u ? 0xffffffffu : ((1u << jhi) - 1u)) & ~(jlo >= 32u ? 0xffffffffu : ((1u << jlo) - 1u));
+  }
+  float run = 0.f;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    uint32_t c[CV::kPer];
+    CV::unpack(raw_v[v], c);
+#pragma unroll
+    for (int q = 0; q < CV::kPer / 4; ++q) {
+      float o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int j = v * CV::kPer + q * 4 + t;
+        float g;
+        if (MASKED) {
+          g = 0.f;
+          if ((vmask >> j) & 1u) g = XSMEM ? xs[c[q * 4 + t]] : __ldg(x + c[q * 4 + t]);
+        } else {
+          g = XSMEM ? xs[c[q * 4 + t]] : __ldg(x + c[q * 4 + t]);
+        }
+        run += g;
+        o[t] = run;
+      }
+      const int jq = (v * CV::kPer + q * 4) >> 2;
+      *reinterpret_cast<float4 *>(pre + jq * 128 + lane * 4) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+  return run;
+}
+
+template <typename ColT, typename PtrT, bool CSER, bool XSMEM>
+__global__ void __launch_bounds__(kMatvecThreads, 1) k_matvec(DotArgs a, const float *__restrict__ x,
+                                                              float *__restrict__ y) {
+  constexpr uint32_t W = kWin;
+  extern __shared__ __align__(16) unsigned char smem[];
+  float *wv = reinterpret_cast<float *>(smem);                 // kSmemValues
+  float *pre_all = wv + kSmemValues;                          // warps x W local prefixes
+  float *off_all = pre_all + kMatvecWarps * W;                // warps x 32 lane offsets
+  float *xs = off_all + kMatvecWarps * 32;                    // n (XSMEM)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float *pre = pre_all + wid * W;
+  float *off = off_all + wid * 32;
+  const ColT *col = static_cast<const ColT *>(a.col);
+  const PtrT *op = static_cast<const PtrT *>(a.op);
+  const uint32_t m = static_cast<uint32_t>(a.m);
+  const uint64_t nw_total = static_cast<uint64_t>(gridDim.x) * kMatvecWarps;
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kMatvecWarps + wid;
+  const uint32_t R0 = static_cast<uint32_t>(gw * m / nw_total), R1 = static_cast<uint32_t>((gw + 1) * m / nw_total);
+  pdl_launch_dependents();  // the next grid may start its own index prologue as our CTAs retire
+
+  // ------------------------------------------------------------ index prologue (encoding only)
+  uint32_t G = R0, rp_l = 0, ep_l = 0;
+  auto load_group = [&](uint32_t g) {
+    const uint32_t idx = g + lane;
+    rp_l = 0;
+    ep_l = 0;
+    if (idx <= R1 && R0 < R1) {
+      rp_l = load_index(a.rp, a.rp_bits, idx);
+      ep_l = ld_idx(op, rp_l);
+    }
+  };
+  load_group(G);
+  const uint32_t s_end = R0 < R1 ? load_index(a.rp, a.rp_bits, R1) : 0u;
+  uint32_t ob = __shfl_sync(0xffffffffu, rp_l, 0);
+  // L2 stream prefetch of this warp's contiguous colI / omegaPtr ranges (TMA engine), tracked in
+  // entries / segments and kept kAheadE entries ahead of the window being processed
+  constexpr uint32_t kChunkE = 4096 / sizeof(ColT), kAheadE = 24576 / sizeof(ColT);
+  constexpr uint32_t kChunkS = 4096 / sizeof(PtrT), kAheadS = 8192 / sizeof(PtrT);
+  const uint32_t e_beg = __shfl_sync(0xffffffffu, ep_l, 0);
+  const uint32_t e_end = R0 < R1 ? ld_idx(op, s_end) : e_beg;
+  uint32_t pf_e = e_beg & ~(16u / sizeof(ColT) - 1u), pf_s = ob & ~(16u / sizeof(PtrT) - 1u);
+  auto stream_prefetch = [&](uint32_t e_pos, uint32_t s_pos) {
+    if (lane == 0) {
+      while (pf_e < e_end && pf_e < e_pos + kAheadE) {
+        const uint32_t ne = min(kChunkE, (e_end - pf_e + 15u) & ~15u);
+        bulk_prefetch_l2(col + pf_e, ne * sizeof(ColT));
+        pf_e += ne;
+      }
+      while (pf_s < s_end && pf_s < s_pos + kAheadS) {
+        const uint32_t ns = min(kChunkS, (s_end - pf_s + 15u) & ~15u);
+        bulk_prefetch_l2(op + pf_s, ns * sizeof(PtrT));
+        pf_s += ns;
+      }
+    }
+  };
+  stream_prefetch(pf_e, pf_s);
+  // omegaPtr FIFO: f[i] = omegaPtr[ob + 32 i + lane] (segment starts), fk[i] = omegaI (CSER)
+  uint32_t f[4];
+  int fk[4];
+  auto fifo_load = [&](uint32_t base, uint32_t &v, int &kk) {
+    const uint32_t s = base + lane;
+    v = s <= s_end ? ld_idx(op, s) : 0xffffffffu;
+    kk = (CSER && s < s_end) ? static_cast<int>(load_index(a.oi, a.oi_bits, s)) : 0;
+  };
+#pragma unroll
+  for (int i = 0; i < 4; ++i) fifo_load(ob + 32u * i, f[i], fk[i]);
+  auto fifo_shift = [&]() {
+    f[0] = f[1]; f[1] = f[2]; f[2] = f[3];
+    fk[0] = fk[1]; fk[1] = fk[2]; fk[2] = fk[3];
+    ob += 32u;
+    fifo_load(ob + 96u, f[3], fk[3]);
+  };
+
+  // ------------------------------------------------------------ wait for the producer of x
+  pdl_wait();
+  const int kv = static_cast<int>(min64(a.k, kSmemValues));
+  for (int i = threadIdx.x; i < kv; i += blockDim.x) wv[i] = static_cast<float>(__ldg(a.omega + i) - a.bg);
+  if (XSMEM) {
+    const int64_t n4 = a.n >> 2;
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+      const float4 *x4 = reinterpret_cast<const float4 *>(x);
+      float4 *xs4 = reinterpret_cast<float4 *>(xs);
+      for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) xs4[i] = __ldg(x4 + i);
+      for (int64_t i = (n4 << 2) + threadIdx.x; i < a.n; i += blockDim.x) xs[i] = __ldg(x + i);
+    } else {
+      for (int64_t i = threadIdx.x; i < a.n; i += blockDim.x) xs[i] = __ldg(x + i);
+    }
+  }
+  __syncthreads();
+
+  constexpr uint32_t kAlign = ColVec<ColT>::kPer;
+  constexpr int NV = kEPL / ColVec<ColT>::kPer;
+  // one-window-ahead register prefetch of colI: (nrow, nw0) is the window after the current one
+  auto load_window = [&](uint32_t wb, uint32_t e1, uint4 *dst) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const uint32_t vp = wb + lane * kEPL + v * ColVec<ColT>::kPer;
+      dst[v] = vp < e1 ? ld_stream(col + vp) : make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+  uint4 nxt[NV];
+  uint32_t nxt_base = 0xffffffffu;  // window base nxt holds (kept exact: empty rows are skipped on use)
+  if (R0 < R1) {
+    const uint32_t e0 = __shfl_sync(0xffffffffu, ep_l, 0), e1 = __shfl_sync(0xffffffffu, ep_l, 1);
+    nxt_base = e0 & ~(kAlign - 1);
+    load_window(nxt_base, e1, nxt);
+  }
+  uint32_t sc = ob;
+  for (uint32_t row = R0; row < R1; ++row) {
+    if (row >= G + 31) {  // next group of rows (only when a warp owns > 31 rows)
+      G = row;
+      load_group(G);
+      nxt_base = __shfl_sync(0xffffffffu, ep_l, 0) & ~(kAlign - 1);
+      load_window(nxt_base, __shfl_sync(0xffffffffu, ep_l, 1), nxt);
+    }
+    const uint32_t s0 = __shfl_sync(0xffffffffu, rp_l, static_cast<int>(row - G));
+    const uint32_t s1 = __shfl_sync(0xffffffffu, rp_l, static_cast<int>(row - G + 1));
+    const uint32_t e0 = __shfl_sync(0xffffffffu, ep_l, static_cast<int>(row - G));
+    const uint32_t e1 = __shfl_sync(0xffffffffu, ep_l, static_cast<int>(row - G + 1));
+    sc = s0;
+    while (sc >= ob + 32u) fifo_shift();
+    float acc = 0.f;
+    float carry = 0.f;  // partial sum of the segment still open at the window end
+    for (uint32_t w0 = e0 & ~(kAlign - 1); w0 < e1; w0 += W) {
+      const uint32_t wn = w0 + W;
+      stream_prefetch(w0, ob);
+      uint4 cur[NV];
+      if (nxt_base == w0) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) cur[v] = nxt[v];
+      } else {
+        load_window(w0, e1, cur);
+      }
+      // prefetch the next window: rest of this row, else the first window of the next row in the group
+      nxt_base = 0xffffffffu;
+      if (wn < e1) {
+        nxt_base = wn;
+        load_window(wn, e1, nxt);
+      } else if (row + 1 < R1 && row + 1 < G + 31) {
+        const uint32_t ne0 = __shfl_sync(0xffffffffu, ep_l, static_cast<int>(row + 1 - G));
+        const uint32_t ne1 = __shfl_sync(0xffffffffu, ep_l, static_cast<int>(row + 2 - G));
+        nxt_base = ne0 & ~(kAlign - 1);
+        load_window(nxt_base, ne1, nxt);
+      }
+      // ---- gather x, this lane's local prefix sums -> smem
+      const float run = (w0 >= e0 && wn <= e1)
+                            ? gather_prefix<ColT, XSMEM, false>(cur, w0, e0, e1, xs, x, pre, lane)
+                            : gather_prefix<ColT, XSMEM, true>(cur, w0, e0, e1, xs, x, pre, lane);
+      float incl = run;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const float t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+      }
+      const float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+      off[lane] = lane ? excl : 0.f;
+      __syncwarp();
+      // ---- segments overlapping this window: one lane per segment
+      for (;;) {
+        const uint32_t s = ob + lane;
+        const uint32_t st = f[0];
+        const uint32_t nx = __shfl_sync(0xffffffffu, f[1], 0);
+        uint32_t en = __shfl_down_sync(0xffffffffu, f[0], 1);
+        if (lane == 31) en = nx;
+        const bool take = s >= sc && s < s1 && st < wn;
+        const bool done = take && en <= wn;
+        const bool live = take && en > st;
+        float total = 0.f;
+        if (live) {
+          const uint32_t lo = st > w0 ? st - w0 : 0u;
+          const uint32_t b = (en < wn ? en - w0 : W) - 1u;
+          const float pb = pre[ppos(b)];
+          if (lo == 0u) {
+            total = off[b >> 5] + pb;
+            if (st < w0) total = carry + total;  // the segment continued from the previous window
+          } else {
+            const uint32_t a0 = lo - 1u;
+            const float pa = pre[ppos(a0)];
+            total = ((a0 >> 5) == (b >> 5)) ? pb - pa : (off[b >> 5] + pb) - (off[a0 >> 5] + pa);
+          }
+          if (done) acc = fmaf(wv[CSER ? fk[0] : static_cast<int>(s - s0 + 1)], total, acc);
+        }
+        const unsigned done_m = __ballot_sync(0xffffffffu, done);
+        const unsigned open_m = __ballot_sync(0xffffffffu, live && !done);
+        if (open_m) carry = __shfl_sync(0xffffffffu, total, __ffs(open_m) - 1);
+        sc += __popc(done_m);
+        if (sc < ob + 32u) break;
+        fifo_shift();
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[row] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + a.bg * a.colsum[0]) : acc;
+  }
+}
+
+// Generic mat-vec for alphabets beyond the u16 slot table: warp per row, lanes over segments.
 template <typename ColT, typename PtrT, bool CSER>
-__global__ void __launch_bounds__(256) k_dot_vec(DotArgs a, const float *__restrict__ x, float *__restrict__ y) {
+__global__ void __launch_bounds__(256) k_matvec_generic(DotArgs a, const float *__restrict__ x,
+                                                        float *__restrict__ y) {
   const ColT *col = static_cast<const ColT *>(a.col);
   const PtrT *op = static_cast<const PtrT *>(a.op);
   const int lane = threadIdx.x & 31;
@@ -59,7 +378,8 @@ __global__ void __launch_bounds__(256) k_dot_vec(DotArgs a, const float *__restr
       if (e1 > e0) {
         float sum = 0.f;
         for (int64_t i = e0; i < e1; ++i) sum += __ldg(x + ld_idx(col, i));
-        acc = fmaf(seg_value(a, CSER, s, s0), sum, acc);
+        const int64_t k = CSER ? static_cast<int64_t>(load_index(a.oi, a.oi_bits, s)) : (s - s0 + 1);
+        acc = fmaf(static_cast<float>(__ldg(a.omega + k) - a.bg), sum, acc);
       }
     }
 #pragma unroll
@@ -68,53 +388,110 @@ __global__ void __launch_bounds__(256) k_dot_vec(DotArgs a, const float *__restr
   }
 }
 
-// Mat-mat: warp per row, lanes across V-wide column groups of the batch.
+template <int V>
+struct XVec {
+  float v[V];
+};
+
+template <int V>
+__device__ __forceinline__ XVec<V> ld_x(const float *p, int64_t cb, int64_t batch) {
+  XVec<V> r;
+  if (V == 4 && cb + 4 <= batch) {
+    const float4 t = __ldg(reinterpret_cast<const float4 *>(p));
+    r.v[0] = t.x; r.v[1] = t.y; r.v[2] = t.z; r.v[V - 1] = t.w;
+  } else if (V == 2 && cb + 2 <= batch) {
+    const float2 t = __ldg(reinterpret_cast<const float2 *>(p));
+    r.v[0] = t.x; r.v[V - 1] = t.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < V; ++j) r.v[j] = (cb + j < batch) ? __ldg(p + j) : 0.f;
+  }
+  return r;
+}
+
+// Mat-mat: warp per (row, 32*V columns of the batch).
 template <typename ColT, typename PtrT, bool CSER, int V>
-__global__ void __launch_bounds__(256) k_dot_mat(DotArgs a, const float *__restrict__ x, int64_t ldx, int64_t batch,
-                                                 float *__restrict__ y, int64_t ldy) {
+__global__ void __launch_bounds__(256) k_matmat(DotArgs a, const float *__restrict__ x, int64_t ldx, int64_t batch,
+                                                float *__restrict__ y, int64_t ldy) {
+  __shared__ int slot_all[8][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int *slots = slot_all[wid];
   const ColT *col = static_cast<const ColT *>(a.col);
   const PtrT *op = static_cast<const PtrT *>(a.op);
-  const int lane = threadIdx.x & 31;
+  const int64_t chunks = ceil_div(batch, 32 * V);
+  const int64_t units = a.m * chunks;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < a.m; row += nwarps) {
+  for (int64_t u = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < units; u += nwarps) {
+    const int64_t row = u / chunks, cb = (u - row * chunks) * 32 * V + lane * V;
     const int64_t s0 = load_index(a.rp, a.rp_bits, row), s1 = load_index(a.rp, a.rp_bits, row + 1);
-    for (int64_t c0 = 0; c0 < batch; c0 += 32 * V) {
-      const int64_t cb = c0 + lane * V;
-      const bool full = cb + V <= batch;
-      float acc[V];
+    float acc[V], sum[V];
 #pragma unroll
-      for (int j = 0; j < V; ++j) acc[j] = 0.f;
-      for (int64_t s = s0; s < s1; ++s) {
-        const int64_t e0 = ld_idx(op, s), e1 = ld_idx(op, s + 1);
-        if (e1 <= e0) continue;
-        float sum[V];
+    for (int j = 0; j < V; ++j) acc[j] = sum[j] = 0.f;
+    int cur_k = -1;
+    if (s1 > s0) {
+      const int64_t e0 = ld_idx(op, s0), e1 = ld_idx(op, s1);
+      int64_t sc = s0;
+      const float *xb = x + cb;
+      for (int64_t base = e0; base < e1; base += 32) {
+        const int64_t wn = base + 32;
+        slots[lane] = -1;
+        __syncwarp();
+        for (;;) {
+          const int64_t s = sc + lane;
+          const bool in_row = s < s1;
+          const int64_t st = in_row ? static_cast<int64_t>(ld_idx(op, s)) : INT64_MAX;
+          const int64_t en = in_row ? static_cast<int64_t>(ld_idx(op, s + 1)) : INT64_MAX;
+          const bool here = st < wn;
+          if (here && en > st)
+            slots[st - base] = CSER ? static_cast<int>(load_index(a.oi, a.oi_bits, s)) : static_cast<int>(s - s0 + 1);
+          const int cnt = __popc(__ballot_sync(0xffffffffu, here));
+          sc += cnt;
+          if (cnt < 32) break;
+        }
+        __syncwarp();
+        const int ne = static_cast<int>(min64(32, e1 - base));
+        const uint32_t my_col = lane < ne ? ld_idx(col, base + lane) : 0u;
+        const int my_k = slots[lane];
+        for (int j0 = 0; j0 < ne; j0 += 8) {
+          XVec<V> xv[8];
 #pragma unroll
-        for (int j = 0; j < V; ++j) sum[j] = 0.f;
-        for (int64_t i = e0; i < e1; ++i) {
-          const float *xr = x + static_cast<int64_t>(ld_idx(col, i)) * ldx + cb;
-          if (V == 4 && full) {
-            const float4 v = __ldg(reinterpret_cast<const float4 *>(xr));
-            sum[0] += v.x; sum[1] += v.y; sum[2] += v.z; sum[V - 1] += v.w;
-          } else if (V == 2 && full) {
-            const float2 v = __ldg(reinterpret_cast<const float2 *>(xr));
-            sum[0] += v.x; sum[V - 1] += v.y;
-          } else {
+          for (int t = 0; t < 8; ++t) {
+            const uint32_t c = __shfl_sync(0xffffffffu, my_col, j0 + t);
+            if (j0 + t < ne) xv[t] = ld_x<V>(xb + static_cast<int64_t>(c) * ldx, cb, batch);
+          }
 #pragma unroll
-            for (int j = 0; j < V; ++j)
-              if (cb + j < batch) sum[j] += __ldg(xr + j);
+          for (int t = 0; t < 8; ++t) {
+            const int k = __shfl_sync(0xffffffffu, my_k, j0 + t);
+            if (j0 + t < ne) {
+              if (k >= 0) {
+                if (cur_k >= 0) {
+                  const float sv = cur_k < 0 ? 0.f : static_cast<float>(__ldg(a.omega + cur_k) - a.bg);
+#pragma unroll
+                  for (int q = 0; q < V; ++q) acc[q] = fmaf(sv, sum[q], acc[q]);
+                }
+#pragma unroll
+                for (int q = 0; q < V; ++q) sum[q] = 0.f;
+                cur_k = k;
+              }
+#pragma unroll
+              for (int q = 0; q < V; ++q) sum[q] += xv[t].v[q];
+            }
           }
         }
-        const float v = seg_value(a, CSER, s, s0);
-#pragma unroll
-        for (int j = 0; j < V; ++j) acc[j] = fmaf(v, sum[j], acc[j]);
+        __syncwarp();
       }
-      float *yr = y + row * ldy;
+      if (cur_k >= 0) {
+        const float sv = static_cast<float>(__ldg(a.omega + cur_k) - a.bg);
 #pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const int64_t c = cb + j;
-        if (c < batch)
-          yr[c] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc[j]) + a.bg * a.colsum[c]) : acc[j];
+        for (int q = 0; q < V; ++q) acc[q] = fmaf(sv, sum[q], acc[q]);
       }
+    }
+    float *yr = y + row * ldy;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int64_t c = cb + j;
+      if (c < batch)
+        yr[c] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc[j]) + a.bg * a.colsum[c]) : acc[j];
     }
   }
 }
@@ -155,23 +532,60 @@ __global__ void __launch_bounds__(1024) k_vecsum(const float *__restrict__ x, in
   }
 }
 
+size_t matvec_smem(int64_t n, bool xsmem) {
+  return kSmemValues * sizeof(float) + kMatvecWarps * kWin * sizeof(float) + kMatvecWarps * 32 * sizeof(float) +
+         (xsmem ? static_cast<size_t>(n) * sizeof(float) : 0);
+}
+
+template <typename ColT, typename PtrT, bool CSER, bool XSMEM>
+int launch_matvec(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
+  const size_t smem = matvec_smem(a.n, XSMEM);
+  auto kern = k_matvec<ColT, PtrT, CSER, XSMEM>;
+  CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CERDOT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMatvecThreads, smem));
+  per_sm = std::max(1, per_sm);
+  const int grid = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(int64_t(num_sms()) * per_sm, ceil_div(a.m, kMatvecWarps))));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kMatvecThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CERDOT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a, x, y));
+  return CERDOT_OK;
+}
+
 template <typename ColT, typename PtrT, bool CSER>
 int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy, cudaStream_t st) {
-  const int64_t warps_per_block = 8;
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.m, warps_per_block),
-                                                                           static_cast<int64_t>(num_sms()) * 64)));
-  if (batch == 1) {
-    k_dot_vec<ColT, PtrT, CSER><<<grid, 256, 0, st>>>(a, x, y);
-  } else {
-    const bool al4 = (ldx % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
-    const bool al2 = (ldx % 2 == 0) && (reinterpret_cast<uintptr_t>(x) % 8 == 0);
-    if (batch >= 128 && al4)
-      k_dot_mat<ColT, PtrT, CSER, 4><<<grid, 256, 0, st>>>(a, x, ldx, batch, y, ldy);
-    else if (batch >= 64 && al2)
-      k_dot_mat<ColT, PtrT, CSER, 2><<<grid, 256, 0, st>>>(a, x, ldx, batch, y, ldy);
-    else
-      k_dot_mat<ColT, PtrT, CSER, 1><<<grid, 256, 0, st>>>(a, x, ldx, batch, y, ldy);
+  if (batch == 1 && (a.m >= (int64_t(1) << 31) || a.k > kSmemValues)) {
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.m, 8), int64_t(num_sms()) * 16)));
+    k_matvec_generic<ColT, PtrT, CSER><<<grid, 256, 0, st>>>(a, x, y);
+    CERDOT_LAUNCH_CHECK();
+    return CERDOT_OK;
   }
+  if (batch == 1) {
+    const bool xsmem = matvec_smem(a.n, true) <= static_cast<size_t>(kMaxSmemBytes);
+    return xsmem ? launch_matvec<ColT, PtrT, CSER, true>(a, x, y, st)
+                 : launch_matvec<ColT, PtrT, CSER, false>(a, x, y, st);
+  }
+  const bool al4 = (ldx % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  const bool al2 = (ldx % 2 == 0) && (reinterpret_cast<uintptr_t>(x) % 8 == 0);
+  const int V = (batch > 64 && al4) ? 4 : ((batch > 32 && al2) ? 2 : 1);
+  const int64_t units = a.m * ceil_div(batch, 32 * V);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(units, 8),
+                                                                           int64_t(num_sms()) * 8)));
+  if (V == 4)
+    k_matmat<ColT, PtrT, CSER, 4><<<grid, 256, 0, st>>>(a, x, ldx, batch, y, ldy);
+  else if (V == 2)
+    k_matmat<ColT, PtrT, CSER, 2><<<grid, 256, 0, st>>>(a, x, ldx, batch, y, ldy);
+  else
+    k_matmat<ColT, PtrT, CSER, 1><<<grid, 256, 0, st>>>(a, x, ldx, batch, y, ldy);
   CERDOT_LAUNCH_CHECK();
   return CERDOT_OK;
 }
@@ -211,6 +625,7 @@ int dot(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, fl
   a.oi_bits = mat->omega_index_bits;
   a.m = mat->m;
   a.n = mat->n;
+  a.k = mat->k;
   a.bg = mat->background;
   if (a.m == 0 || batch == 0) return CERDOT_OK;
   if (a.bg != 0.0) {
