@@ -34,6 +34,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -58,6 +59,7 @@ struct DotArgs {
   int64_t m, n, k;
   double bg;
   const double *colsum;  // batch doubles when bg != 0
+  int64_t segs;          // segment count (omegaPtr has segs + 1 entries)
 };
 
 template <typename T>
@@ -165,47 +167,85 @@ __device__ __forceinline__ float gather_prefix(const uint4 *raw_v, uint32_t w0, 
   return run;
 }
 
-template <typename ColT, typename PtrT, bool CSER, bool XSMEM>
-__global__ void __launch_bounds__(kMatvecThreads, 1) k_matvec(DotArgs a, const float *__restrict__ x,
-                                                              float *__restrict__ y) {
+constexpr int kFifoDepth = 4;
+
+__device__ __forceinline__ void cp_async4(void *smem_dst, const void *gmem_src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Shared-memory carve-up of k_matvec (byte offsets; all 16 B aligned).
+struct MatvecSmem {
+  uint32_t wv, pre, off, ring_op, ring_oi, xs, total;
+};
+__host__ __device__ __forceinline__ MatvecSmem matvec_layout(int64_t k, int64_t n_smem, uint32_t warps) {
+  MatvecSmem L{};
+  uint32_t o = 0;
+  auto take = [&](uint32_t bytes) {
+    const uint32_t r = o;
+    o += (bytes + 15u) & ~15u;
+    return r;
+  };
+  L.wv = take(static_cast<uint32_t>(min64(k, kSmemValues)) * 4u);
+  L.pre = take(warps * kWin * 4u);
+  L.off = take(warps * 32u * 4u);
+  L.ring_op = take(warps * kFifoDepth * 128u);
+  L.ring_oi = take(warps * kFifoDepth * 128u);
+  L.xs = take(static_cast<uint32_t>(n_smem) * 4u);
+  L.total = o;
+  return L;
+}
+
+template <typename ColT, typename PtrT, bool CSER, bool XSMEM, int NT, int NBUF>
+__global__ void __launch_bounds__(NT, 1) k_matvec(DotArgs a, const float *__restrict__ x, float *__restrict__ y) {
+  constexpr int kWarps = NT / 32;
+  using CV = ColVec<ColT>;
   constexpr uint32_t W = kWin;
+  constexpr int NV = kEPL / CV::kPer;
+  constexpr uint32_t kAlign = CV::kPer;
+  constexpr int D = kFifoDepth;
   extern __shared__ __align__(16) unsigned char smem[];
-  float *wv = reinterpret_cast<float *>(smem);                 // kSmemValues
-  float *pre_all = wv + kSmemValues;                          // warps x W local prefixes
-  float *off_all = pre_all + kMatvecWarps * W;                // warps x 32 lane offsets
-  float *xs = off_all + kMatvecWarps * 32;                    // n (XSMEM)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  float *pre = pre_all + wid * W;
-  float *off = off_all + wid * 32;
+  MatvecSmem L = matvec_layout(a.k, XSMEM ? a.n : 0, kWarps);
+  float *wv = reinterpret_cast<float *>(smem + L.wv);
+  float *pre = reinterpret_cast<float *>(smem + L.pre) + wid * W;
+  float *off = reinterpret_cast<float *>(smem + L.off) + wid * 32;
+  unsigned char *ring_op = smem + L.ring_op + wid * D * 128;
+  unsigned char *ring_oi = smem + L.ring_oi + wid * D * 128;
+  float *xs = reinterpret_cast<float *>(smem + L.xs);
   const ColT *col = static_cast<const ColT *>(a.col);
   const PtrT *op = static_cast<const PtrT *>(a.op);
   const uint32_t m = static_cast<uint32_t>(a.m);
-  const uint64_t nw_total = static_cast<uint64_t>(gridDim.x) * kMatvecWarps;
-  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kMatvecWarps + wid;
+  const uint64_t nw_total = static_cast<uint64_t>(gridDim.x) * kWarps;
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kWarps + wid;
   const uint32_t R0 = static_cast<uint32_t>(gw * m / nw_total), R1 = static_cast<uint32_t>((gw + 1) * m / nw_total);
   pdl_launch_dependents();  // the next grid may start its own index prologue as our CTAs retire
 
-  // ------------------------------------------------------------ index prologue (encoding only)
-  uint32_t G = R0, rp_l = 0, ep_l = 0;
+  // ------------------------------------------------------------ row groups (31 rows per lane-register group)
+  uint32_t gG = R0, g_rp = 0, g_ep = 0;
   auto load_group = [&](uint32_t g) {
+    gG = g;
     const uint32_t idx = g + lane;
-    rp_l = 0;
-    ep_l = 0;
+    g_rp = 0;
+    g_ep = 0;
     if (idx <= R1 && R0 < R1) {
-      rp_l = load_index(a.rp, a.rp_bits, idx);
-      ep_l = ld_idx(op, rp_l);
+      g_rp = load_index(a.rp, a.rp_bits, idx);
+      g_ep = ld_idx(op, g_rp);
     }
   };
-  load_group(G);
-  const uint32_t s_end = R0 < R1 ? load_index(a.rp, a.rp_bits, R1) : 0u;
-  uint32_t ob = __shfl_sync(0xffffffffu, rp_l, 0);
-  // L2 stream prefetch of this warp's contiguous colI / omegaPtr ranges (TMA engine), tracked in
-  // entries / segments and kept kAheadE entries ahead of the window being processed
+  load_group(R0);
+  const uint32_t s_beg = __shfl_sync(0xffffffffu, g_rp, 0);
+  const uint32_t s_end = R0 < R1 ? load_index(a.rp, a.rp_bits, R1) : s_beg;
+  const uint32_t e_beg = __shfl_sync(0xffffffffu, g_ep, 0);
+  const uint32_t e_end = R0 < R1 ? ld_idx(op, s_end) : e_beg;
+
+  // ------------------------------------------------------------ L2 stream prefetch (TMA engine)
   constexpr uint32_t kChunkE = 4096 / sizeof(ColT), kAheadE = 24576 / sizeof(ColT);
   constexpr uint32_t kChunkS = 4096 / sizeof(PtrT), kAheadS = 8192 / sizeof(PtrT);
-  const uint32_t e_beg = __shfl_sync(0xffffffffu, ep_l, 0);
-  const uint32_t e_end = R0 < R1 ? ld_idx(op, s_end) : e_beg;
-  uint32_t pf_e = e_beg & ~(16u / sizeof(ColT) - 1u), pf_s = ob & ~(16u / sizeof(PtrT) - 1u);
+  uint32_t pf_e = e_beg & ~(16u / sizeof(ColT) - 1u), pf_s = s_beg & ~(16u / sizeof(PtrT) - 1u);
   auto stream_prefetch = [&](uint32_t e_pos, uint32_t s_pos) {
     if (lane == 0) {
       while (pf_e < e_end && pf_e < e_pos + kAheadE) {
@@ -221,22 +261,97 @@ __global__ void __launch_bounds__(kMatvecThreads, 1) k_matvec(DotArgs a, const f
     }
   };
   stream_prefetch(pf_e, pf_s);
-  // omegaPtr FIFO: f[i] = omegaPtr[ob + 32 i + lane] (segment starts), fk[i] = omegaI (CSER)
-  uint32_t f[4];
-  int fk[4];
-  auto fifo_load = [&](uint32_t base, uint32_t &v, int &kk) {
-    const uint32_t s = base + lane;
-    v = s <= s_end ? ld_idx(op, s) : 0xffffffffu;
-    kk = (CSER && s < s_end) ? static_cast<int>(load_index(a.oi, a.oi_bits, s)) : 0;
+
+  // ------------------------------------------------------------ segment FIFO: smem ring filled by cp.async
+  // batch t holds omegaPtr[fb + 32t .. +32) (raw PtrT) and omegaI of the same segments (CSER)
+  const uint32_t fb = s_beg & ~31u;
+  uint32_t ft = 0;                      // batch being consumed
+  auto fifo_issue = [&](uint32_t tt) {
+    const uint32_t base = fb + 32u * tt;
+    const int slot = static_cast<int>(tt % D);
+    constexpr uint32_t per = 4u / sizeof(PtrT) ? 4u / sizeof(PtrT) : 1u;  // entries per 4 B chunk
+    const uint32_t nchunks = 32u / per;
+    if (static_cast<uint32_t>(lane) < nchunks) {
+      const uint32_t e = base + lane * per;
+      if (e <= static_cast<uint32_t>(a.segs) && base <= s_end)
+        cp_async4(ring_op + slot * 128 + lane * 4, op + e);
+    }
+    if (CSER) {
+      const uint32_t ob_bytes = a.oi_bits / 8;
+      const uint32_t per_oi = 4u / ob_bytes, nch = 32u / per_oi;
+      if (static_cast<uint32_t>(lane) < nch) {
+        const uint32_t e = base + lane * per_oi;
+        if (e < static_cast<uint32_t>(a.segs) && base < s_end)
+          cp_async4(ring_oi + slot * 128 + lane * 4, static_cast<const unsigned char *>(a.oi) + e * ob_bytes);
+      }
+    }
+    cp_async_commit();
   };
 #pragma unroll
-  for (int i = 0; i < 4; ++i) fifo_load(ob + 32u * i, f[i], fk[i]);
+  for (int i = 0; i < D; ++i) fifo_issue(i);
   auto fifo_shift = [&]() {
-    f[0] = f[1]; f[1] = f[2]; f[2] = f[3];
-    fk[0] = fk[1]; fk[1] = fk[2]; fk[2] = fk[3];
-    ob += 32u;
-    fifo_load(ob + 96u, f[3], fk[3]);
+    fifo_issue(ft + D);
+    ++ft;
   };
+  // the ring is a circular buffer of D*32 consecutive segments: segment s sits at (s - fb) % (32 D)
+  // inside its batch's 128 B slot (entries of PtrT / omegaI width)
+  auto ring_ptr = [&](uint32_t s) -> uint32_t {
+    const uint32_t r = (s - fb) % (32u * D);
+    return reinterpret_cast<const PtrT *>(ring_op + (r >> 5) * 128)[r & 31u];
+  };
+  auto ring_oi_val = [&](uint32_t s) -> int {
+    const uint32_t r = (s - fb) % (32u * D);
+    const unsigned char *slot = ring_oi + (r >> 5) * 128;
+    switch (a.oi_bits) {
+      case 8: return slot[r & 31u];
+      case 16: return reinterpret_cast<const uint16_t *>(slot)[r & 31u];
+      default: return static_cast<int>(reinterpret_cast<const uint32_t *>(slot)[r & 31u]);
+    }
+  };
+
+  // ------------------------------------------------------------ window generator (runs 3 windows ahead)
+  struct Win {
+    uint32_t row, w0, s0, s1, e0, e1;
+  };
+  uint32_t g_row = R0, g_w0 = 0;
+  auto row_meta = [&](uint32_t r, Win &w) {
+    w.row = r;
+    w.s0 = __shfl_sync(0xffffffffu, g_rp, static_cast<int>(r - gG));
+    w.s1 = __shfl_sync(0xffffffffu, g_rp, static_cast<int>(r - gG + 1));
+    w.e0 = __shfl_sync(0xffffffffu, g_ep, static_cast<int>(r - gG));
+    w.e1 = __shfl_sync(0xffffffffu, g_ep, static_cast<int>(r - gG + 1));
+  };
+  Win gcur;  // metadata of the generator's current row
+  auto seek_row = [&](uint32_t r) {  // first non-empty row >= r (rows of entries; empty rows are emitted by the consumer)
+    for (; r < R1; ++r) {
+      if (r >= gG + 31) load_group(r);
+      row_meta(r, gcur);
+      if (gcur.e1 > gcur.e0) break;
+    }
+    g_row = r;
+    g_w0 = r < R1 ? (gcur.e0 & ~(kAlign - 1)) : 0u;
+  };
+  seek_row(R0);
+  auto gen = [&](Win &w, uint4 *buf) {
+    w = gcur;
+    w.row = g_row;
+    w.w0 = g_w0;
+    if (g_row >= R1) return;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const uint32_t vp = g_w0 + lane * kEPL + v * CV::kPer;
+      buf[v] = vp < gcur.e1 ? ld_stream(col + vp) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    if (g_w0 + W < gcur.e1) g_w0 += W;
+    else seek_row(g_row + 1);
+  };
+  Win ma, mb, mc;
+  uint4 A[NV], B[NV], C[NV];
+  gen(ma, A);
+  if (NBUF > 1) {
+    gen(mb, B);
+    gen(mc, C);
+  }
 
   // ------------------------------------------------------------ wait for the producer of x
   pdl_wait();
@@ -254,112 +369,99 @@ __global__ void __launch_bounds__(kMatvecThreads, 1) k_matvec(DotArgs a, const f
     }
   }
   __syncthreads();
+  const float y_empty = a.bg != 0.0 ? static_cast<float>(a.bg * a.colsum[0]) : 0.f;
 
-  constexpr uint32_t kAlign = ColVec<ColT>::kPer;
-  constexpr int NV = kEPL / ColVec<ColT>::kPer;
-  // one-window-ahead register prefetch of colI: (nrow, nw0) is the window after the current one
-  auto load_window = [&](uint32_t wb, uint32_t e1, uint4 *dst) {
+  // ------------------------------------------------------------ consumer
+  uint32_t next_emit = R0;  // first row whose y is not written yet
+  float acc = 0.f, carry = 0.f;
+  uint32_t sc = 0;
+  auto emit_empty = [&](uint32_t upto) {
+    for (uint32_t r = next_emit + lane; r < upto; r += 32) y[r] = y_empty;
+    next_emit = max(next_emit, upto);
+  };
+  auto process = [&](const uint4 *cur, const Win &w) {
+    if (w.w0 == (w.e0 & ~(kAlign - 1))) {  // first window of the row
+      emit_empty(w.row);
+      acc = 0.f;
+      carry = 0.f;
+      sc = w.s0;
+      while (sc >= fb + 32u * (ft + 1)) fifo_shift();
+    }
+    const uint32_t w0 = w.w0, wn = w0 + W;
+    stream_prefetch(w0, fb + 32u * ft);
+    const float run = (w0 >= w.e0 && wn <= w.e1)
+                          ? gather_prefix<ColT, XSMEM, false>(cur, w0, w.e0, w.e1, xs, x, pre, lane)
+                          : gather_prefix<ColT, XSMEM, true>(cur, w0, w.e0, w.e1, xs, x, pre, lane);
+    float incl = run;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const uint32_t vp = wb + lane * kEPL + v * ColVec<ColT>::kPer;
-      dst[v] = vp < e1 ? ld_stream(col + vp) : make_uint4(0u, 0u, 0u, 0u);
+    for (int d = 1; d < 32; d <<= 1) {
+      const float t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += t;
+    }
+    const float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    off[lane] = lane ? excl : 0.f;
+    // ---- segments overlapping this window: one lane per segment
+    for (;;) {
+      cp_async_wait<D - 2>();  // batches ft and ft+1 hold segments [sc, sc + 32]
+      __syncwarp();
+      const uint32_t s = sc + lane;
+      const uint32_t st = ring_ptr(s);
+      const uint32_t en = ring_ptr(s + 1);
+      const bool take = s < w.s1 && st < wn;
+      const bool done = take && en <= wn;
+      const bool live = take && en > st;
+      float total = 0.f;
+      if (live) {
+        const uint32_t lo = st > w0 ? st - w0 : 0u;
+        const uint32_t b = (en < wn ? en - w0 : W) - 1u;
+        const float pb = pre[ppos(b)];
+        if (lo == 0u) {
+          total = off[b >> 5] + pb;
+          if (st < w0) total = carry + total;  // the segment continued from the previous window
+        } else {
+          const uint32_t a0 = lo - 1u;
+          const float pa = pre[ppos(a0)];
+          total = ((a0 >> 5) == (b >> 5)) ? pb - pa : (off[b >> 5] + pb) - (off[a0 >> 5] + pa);
+        }
+        if (done) acc = fmaf(wv[CSER ? ring_oi_val(s) : static_cast<int>(s - w.s0 + 1)], total, acc);
+      }
+      const unsigned done_m = __ballot_sync(0xffffffffu, done);
+      const unsigned open_m = __ballot_sync(0xffffffffu, live && !done);
+      if (open_m) carry = __shfl_sync(0xffffffffu, total, __ffs(open_m) - 1);
+      const int ndone = __popc(done_m);
+      sc += ndone;
+      while (sc >= fb + 32u * (ft + 1)) fifo_shift();
+      if (ndone < 32) break;
+    }
+    __syncwarp();
+    if (wn >= w.e1) {  // last window of the row
+      float r = acc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+      if (lane == 0) y[w.row] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(r) + a.bg * a.colsum[0]) : r;
+      next_emit = w.row + 1;
     }
   };
-  uint4 nxt[NV];
-  uint32_t nxt_base = 0xffffffffu;  // window base nxt holds (kept exact: empty rows are skipped on use)
-  if (R0 < R1) {
-    const uint32_t e0 = __shfl_sync(0xffffffffu, ep_l, 0), e1 = __shfl_sync(0xffffffffu, ep_l, 1);
-    nxt_base = e0 & ~(kAlign - 1);
-    load_window(nxt_base, e1, nxt);
-  }
-  uint32_t sc = ob;
-  for (uint32_t row = R0; row < R1; ++row) {
-    if (row >= G + 31) {  // next group of rows (only when a warp owns > 31 rows)
-      G = row;
-      load_group(G);
-      nxt_base = __shfl_sync(0xffffffffu, ep_l, 0) & ~(kAlign - 1);
-      load_window(nxt_base, __shfl_sync(0xffffffffu, ep_l, 1), nxt);
+  if (NBUF > 1) {  // three windows in flight, statically rolled (no register moves)
+    for (;;) {
+      if (ma.row >= R1) break;
+      process(A, ma);
+      gen(ma, A);
+      if (mb.row >= R1) break;
+      process(B, mb);
+      gen(mb, B);
+      if (mc.row >= R1) break;
+      process(C, mc);
+      gen(mc, C);
     }
-    const uint32_t s0 = __shfl_sync(0xffffffffu, rp_l, static_cast<int>(row - G));
-    const uint32_t s1 = __shfl_sync(0xffffffffu, rp_l, static_cast<int>(row - G + 1));
-    const uint32_t e0 = __shfl_sync(0xffffffffu, ep_l, static_cast<int>(row - G));
-    const uint32_t e1 = __shfl_sync(0xffffffffu, ep_l, static_cast<int>(row - G + 1));
-    sc = s0;
-    while (sc >= ob + 32u) fifo_shift();
-    float acc = 0.f;
-    float carry = 0.f;  // partial sum of the segment still open at the window end
-    for (uint32_t w0 = e0 & ~(kAlign - 1); w0 < e1; w0 += W) {
-      const uint32_t wn = w0 + W;
-      stream_prefetch(w0, ob);
-      uint4 cur[NV];
-      if (nxt_base == w0) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v) cur[v] = nxt[v];
-      } else {
-        load_window(w0, e1, cur);
-      }
-      // prefetch the next window: rest of this row, else the first window of the next row in the group
-      nxt_base = 0xffffffffu;
-      if (wn < e1) {
-        nxt_base = wn;
-        load_window(wn, e1, nxt);
-      } else if (row + 1 < R1 && row + 1 < G + 31) {
-        const uint32_t ne0 = __shfl_sync(0xffffffffu, ep_l, static_cast<int>(row + 1 - G));
-        const uint32_t ne1 = __shfl_sync(0xffffffffu, ep_l, static_cast<int>(row + 2 - G));
-        nxt_base = ne0 & ~(kAlign - 1);
-        load_window(nxt_base, ne1, nxt);
-      }
-      // ---- gather x, this lane's local prefix sums -> smem
-      const float run = (w0 >= e0 && wn <= e1)
-                            ? gather_prefix<ColT, XSMEM, false>(cur, w0, e0, e1, xs, x, pre, lane)
-                            : gather_prefix<ColT, XSMEM, true>(cur, w0, e0, e1, xs, x, pre, lane);
-      float incl = run;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const float t = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += t;
-      }
-      const float excl = __shfl_up_sync(0xffffffffu, incl, 1);
-      off[lane] = lane ? excl : 0.f;
-      __syncwarp();
-      // ---- segments overlapping this window: one lane per segment
-      for (;;) {
-        const uint32_t s = ob + lane;
-        const uint32_t st = f[0];
-        const uint32_t nx = __shfl_sync(0xffffffffu, f[1], 0);
-        uint32_t en = __shfl_down_sync(0xffffffffu, f[0], 1);
-        if (lane == 31) en = nx;
-        const bool take = s >= sc && s < s1 && st < wn;
-        const bool done = take && en <= wn;
-        const bool live = take && en > st;
-        float total = 0.f;
-        if (live) {
-          const uint32_t lo = st > w0 ? st - w0 : 0u;
-          const uint32_t b = (en < wn ? en - w0 : W) - 1u;
-          const float pb = pre[ppos(b)];
-          if (lo == 0u) {
-            total = off[b >> 5] + pb;
-            if (st < w0) total = carry + total;  // the segment continued from the previous window
-          } else {
-            const uint32_t a0 = lo - 1u;
-            const float pa = pre[ppos(a0)];
-            total = ((a0 >> 5) == (b >> 5)) ? pb - pa : (off[b >> 5] + pb) - (off[a0 >> 5] + pa);
-          }
-          if (done) acc = fmaf(wv[CSER ? fk[0] : static_cast<int>(s - s0 + 1)], total, acc);
-        }
-        const unsigned done_m = __ballot_sync(0xffffffffu, done);
-        const unsigned open_m = __ballot_sync(0xffffffffu, live && !done);
-        if (open_m) carry = __shfl_sync(0xffffffffu, total, __ffs(open_m) - 1);
-        sc += __popc(done_m);
-        if (sc < ob + 32u) break;
-        fifo_shift();
-      }
-      __syncwarp();
+  } else {
+    while (ma.row < R1) {
+      process(A, ma);
+      gen(ma, A);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) y[row] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + a.bg * a.colsum[0]) : acc;
   }
+  emit_empty(R1);
+  cp_async_wait<0>();
 }
 
 // Generic mat-vec for alphabets beyond the u16 slot table: warp per row, lanes over segments.
@@ -532,24 +634,20 @@ __global__ void __launch_bounds__(1024) k_vecsum(const float *__restrict__ x, in
   }
 }
 
-size_t matvec_smem(int64_t n, bool xsmem) {
-  return kSmemValues * sizeof(float) + kMatvecWarps * kWin * sizeof(float) + kMatvecWarps * 32 * sizeof(float) +
-         (xsmem ? static_cast<size_t>(n) * sizeof(float) : 0);
+size_t matvec_smem(int64_t k, int64_t n, bool xsmem, uint32_t warps) {
+  return matvec_layout(k, xsmem ? n : 0, warps).total;
 }
 
-template <typename ColT, typename PtrT, bool CSER, bool XSMEM>
+template <typename ColT, typename PtrT, bool CSER, bool XSMEM, int NT, int NBUF>
 int launch_matvec(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
-  const size_t smem = matvec_smem(a.n, XSMEM);
-  auto kern = k_matvec<ColT, PtrT, CSER, XSMEM>;
+  const size_t smem = matvec_smem(a.k, a.n, XSMEM, NT / 32);
+  auto kern = k_matvec<ColT, PtrT, CSER, XSMEM, NT, NBUF>;
   CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int per_sm = 0;
-  CERDOT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMatvecThreads, smem));
-  per_sm = std::max(1, per_sm);
-  const int grid = static_cast<int>(
-      std::max<int64_t>(1, std::min<int64_t>(int64_t(num_sms()) * per_sm, ceil_div(a.m, kMatvecWarps))));
+  // every SM gets a CTA; rows are split fractionally over all warps (R0 = gw*m/warps)
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms(), a.m)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kMatvecThreads);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -570,9 +668,14 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
     return CERDOT_OK;
   }
   if (batch == 1) {
-    const bool xsmem = matvec_smem(a.n, true) <= static_cast<size_t>(kMaxSmemBytes);
-    return xsmem ? launch_matvec<ColT, PtrT, CSER, true>(a, x, y, st)
-                 : launch_matvec<ColT, PtrT, CSER, false>(a, x, y, st);
+    // 32 warps per SM when x and the per-warp tables fit, else 16 warps with three windows in flight
+    const char *force = getenv("CERDOT_MATVEC_NT");
+    const bool wide = force ? atoi(force) == 1024
+                            : matvec_smem(a.k, a.n, true, 32) <= static_cast<size_t>(kMaxSmemBytes);
+    if (wide) return launch_matvec<ColT, PtrT, CSER, true, 1024, 1>(a, x, y, st);
+    const bool xsmem = matvec_smem(a.k, a.n, true, 16) <= static_cast<size_t>(kMaxSmemBytes);
+    return xsmem ? launch_matvec<ColT, PtrT, CSER, true, 512, 3>(a, x, y, st)
+                 : launch_matvec<ColT, PtrT, CSER, false, 512, 3>(a, x, y, st);
   }
   const bool al4 = (ldx % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
   const bool al2 = (ldx % 2 == 0) && (reinterpret_cast<uintptr_t>(x) % 8 == 0);
@@ -627,6 +730,7 @@ int dot(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, fl
   a.n = mat->n;
   a.k = mat->k;
   a.bg = mat->background;
+  a.segs = mat->segments;
   if (a.m == 0 || batch == 0) return CERDOT_OK;
   if (a.bg != 0.0) {
     if (workspace == nullptr || workspace_bytes < sizeof(double) * static_cast<size_t>(batch))
