@@ -69,13 +69,16 @@ typedef struct {
   int64_t nnz;                /* len(col_index) */
   int64_t segments;           /* len(omega_ptr) - 1 */
   const double *omega;        /* (device) k: CER frequency-major, CSER value-ascending */
-  const void *col_index;      /* (device) nnz unsigned ints of col_bits; readable up to the next
-                                 16-byte boundary past the last entry (vector loads) */
+  const void *col_index;      /* (device) nnz unsigned ints of col_bits.  col_index, omega_ptr and
+                                 omega_index must be readable up to the next 16-byte boundary past
+                                 their last entry (16 B vector loads / TMA bulk copies) */
   const void *omega_ptr;      /* (device) segments+1 unsigned ints of omega_ptr_bits */
   const void *row_ptr;        /* (device) m+1 unsigned ints of row_ptr_bits */
   const void *omega_index;    /* (device) CSER: segments unsigned ints of omega_index_bits */
   int32_t col_bits, omega_ptr_bits, row_ptr_bits, omega_index_bits; /* 8, 16 or 32 */
   double background;          /* host copy of omega[0] (CER) / omega[mode_index] (CSER) */
+  int64_t max_row_nnz;        /* largest row (entries), 0 = unknown; selects the mat-vec tiling */
+  int64_t max_row_segments;   /* largest row (segments), 0 = unknown */
 } cerdot_matrix;
 
 /* Result of phase 1 of the conversion. */
@@ -89,6 +92,9 @@ typedef struct {
   int32_t path;               /* 0 = on-chip hash path (k <= CERDOT_FAST_K), 1 = sort path */
   double background;          /* omega[0] of the CER alphabet */
   size_t workspace_bytes;     /* bytes of workspace the plan+fill need */
+  int64_t max_row_nnz;        /* largest row in entries */
+  int64_t max_row_segments_cer;
+  int64_t max_row_segments_cser;
 } cerdot_encode_info;
 
 #define CERDOT_FAST_K 2048

@@ -41,6 +41,8 @@ class CerdotMatrix(ctypes.Structure):
         ("row_ptr_bits", ctypes.c_int32),
         ("omega_index_bits", ctypes.c_int32),
         ("background", ctypes.c_double),
+        ("max_row_nnz", ctypes.c_int64),
+        ("max_row_segments", ctypes.c_int64),
     ]
 
 
@@ -56,6 +58,9 @@ class CerdotEncodeInfo(ctypes.Structure):
         ("path", ctypes.c_int32),
         ("background", ctypes.c_double),
         ("workspace_bytes", ctypes.c_size_t),
+        ("max_row_nnz", ctypes.c_int64),
+        ("max_row_segments_cer", ctypes.c_int64),
+        ("max_row_segments_cser", ctypes.c_int64),
     ]
 
 

@@ -60,6 +60,7 @@ struct DotArgs {
   double bg;
   const double *colsum;  // batch doubles when bg != 0
   int64_t segs;          // segment count (omegaPtr has segs + 1 entries)
+  int64_t max_row_nnz, max_row_segs;
 };
 
 template <typename T>
@@ -464,6 +465,306 @@ __global__ void __launch_bounds__(NT, 1) k_matvec(DotArgs a, const float *__rest
   cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Mat-vec, CTA-tile pipeline (rows that fit a tile): a persistent CTA owns a block of rows, groups
+// them into tiles of whole rows (<= kTileE entries, <= kTileS segments) and streams each tile's
+// colI / omegaPtr / omegaI ranges into double-buffered shared memory with TMA bulk copies
+// (cp.async.bulk + mbarrier).  Per tile, all threads: (A) gather x from smem and build per-thread
+// prefix sums, (B) a block scan of thread totals, (C) warp-per-row segment sums as hierarchical
+// prefix differences (thread / warp / tile levels, so no long-prefix cancellation), one fma per
+// segment, warp reduction per row.
+constexpr int kTileNT = 512;
+constexpr int kTileWarps = kTileNT / 32;
+constexpr int kTileEPT = 16;                                  // entries per thread (>= 16 B of u8 colI)
+constexpr uint32_t kTileCap = kTileNT * kTileEPT;            // aligned entry slots (8192)
+constexpr uint32_t kTileE = kTileCap - 32;                   // entries per tile (16 B alignment slack)
+constexpr uint32_t kTileS = 2048;                             // segments per tile
+constexpr uint32_t kTileRows = 1024;                          // rows staged per row group
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+struct TileSmem {
+  uint32_t xs, wv, rp, ep, trow, stage, stage_bytes, col_off, op_off, oi_off, pre, tex, tinc, wex, winc, bar, total;
+};
+__host__ __device__ __forceinline__ TileSmem tile_layout(int64_t k, int64_t n, int col_bytes, int ptr_bytes,
+                                                         int oi_bytes) {
+  TileSmem L{};
+  uint32_t o = 0;
+  auto take = [&](uint32_t b) {
+    const uint32_t r = o;
+    o += (b + 15u) & ~15u;
+    return r;
+  };
+  L.bar = take(2 * 8);
+  L.xs = take(static_cast<uint32_t>(n) * 4u);
+  L.wv = take(static_cast<uint32_t>(min64(k, kSmemValues)) * 4u);
+  L.rp = take((kTileRows + 1) * 4u);
+  L.ep = take((kTileRows + 1) * 4u);
+  L.trow = take((kTileRows + 2) * 4u);
+  L.col_off = 0;
+  L.op_off = (kTileCap * col_bytes + 15u) & ~15u;
+  L.oi_off = L.op_off + (((kTileS + 1) * ptr_bytes + 32u + 15u) & ~15u);
+  L.stage_bytes = L.oi_off + ((kTileS * oi_bytes + 32u + 15u) & ~15u);
+  L.stage = take(2 * L.stage_bytes);
+  L.pre = take(kTileCap * 4u);
+  L.tex = take(kTileNT * 4u);
+  L.tinc = take(kTileNT * 4u);
+  L.wex = take(kTileWarps * 4u);
+  L.winc = take(kTileWarps * 4u);
+  L.total = o;
+  return L;
+}
+
+// prefix-table slot of aligned entry q (thread q/EPT, item j=q%EPT): (j/4)*NT*4 + thread*4 + j%4
+__device__ __forceinline__ uint32_t tpos(uint32_t q) {
+  return ((q % kTileEPT) >> 2) * (kTileNT * 4u) + (q / kTileEPT) * 4u + (q & 3u);
+}
+
+template <typename ColT, typename PtrT, bool CSER>
+__global__ void __launch_bounds__(kTileNT, 1) k_matvec_tile(DotArgs a, const float *__restrict__ x,
+                                                            float *__restrict__ y) {
+  using CV = ColVec<ColT>;
+  constexpr int NVT = kTileEPT / CV::kPer;  // 16 B vectors per thread per tile
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int oib = CSER ? a.oi_bits / 8 : 1;
+  const TileSmem L = tile_layout(a.k, a.n, sizeof(ColT), sizeof(PtrT), oib);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L.bar);
+  float *xs = reinterpret_cast<float *>(smem + L.xs);
+  float *wv = reinterpret_cast<float *>(smem + L.wv);
+  uint32_t *rp_s = reinterpret_cast<uint32_t *>(smem + L.rp);
+  uint32_t *ep_s = reinterpret_cast<uint32_t *>(smem + L.ep);
+  uint32_t *trow = reinterpret_cast<uint32_t *>(smem + L.trow);
+  float *pre = reinterpret_cast<float *>(smem + L.pre);
+  float *tex = reinterpret_cast<float *>(smem + L.tex);
+  float *tinc = reinterpret_cast<float *>(smem + L.tinc);
+  float *wex = reinterpret_cast<float *>(smem + L.wex);
+  float *winc = reinterpret_cast<float *>(smem + L.winc);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const ColT *col = static_cast<const ColT *>(a.col);
+  const PtrT *op = static_cast<const PtrT *>(a.op);
+  const unsigned char *oi = static_cast<const unsigned char *>(a.oi);
+  const uint32_t m = static_cast<uint32_t>(a.m);
+  const uint32_t R0 = static_cast<uint32_t>(static_cast<uint64_t>(blockIdx.x) * m / gridDim.x);
+  const uint32_t R1 = static_cast<uint32_t>(static_cast<uint64_t>(blockIdx.x + 1) * m / gridDim.x);
+  pdl_launch_dependents();
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t issued = 0, consumed = 0;  // tiles issued / consumed by this CTA (stage = u % 2)
+  bool staged_x = false;
+  float y_empty = 0.f;
+
+  // TMA issue of one tile (rows [ta, tb) of the current group) into stage u % 2
+  auto issue = [&](uint32_t ta, uint32_t tb, uint32_t u) {
+    unsigned char *st = smem + L.stage + (u & 1u) * L.stage_bytes;
+    const uint32_t Sa = rp_s[ta], Sb = rp_s[tb], Ea = ep_s[ta], Eb = ep_s[tb];
+    const uintptr_t c0 = reinterpret_cast<uintptr_t>(col + Ea) & ~uintptr_t(15);
+    const uintptr_t c1 = (reinterpret_cast<uintptr_t>(col + Eb) + 15) & ~uintptr_t(15);
+    const uintptr_t o0 = reinterpret_cast<uintptr_t>(op + Sa) & ~uintptr_t(15);
+    const uintptr_t o1 = (reinterpret_cast<uintptr_t>(op + Sb + 1) + 15) & ~uintptr_t(15);
+    uintptr_t i0 = 0, i1 = 0;
+    if (CSER && Sb > Sa) {
+      i0 = reinterpret_cast<uintptr_t>(oi + static_cast<size_t>(Sa) * oib) & ~uintptr_t(15);
+      i1 = (reinterpret_cast<uintptr_t>(oi + static_cast<size_t>(Sb) * oib) + 15) & ~uintptr_t(15);
+    }
+    const uint32_t nc = Eb > Ea ? static_cast<uint32_t>(c1 - c0) : 0u;
+    const uint32_t no = static_cast<uint32_t>(o1 - o0), ni = static_cast<uint32_t>(i1 - i0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bar[u & 1u], nc + no + ni);
+    if (nc) bulk_g2s(st + L.col_off, reinterpret_cast<const void *>(c0), nc, &bar[u & 1u]);
+    bulk_g2s(st + L.op_off, reinterpret_cast<const void *>(o0), no, &bar[u & 1u]);
+    if (ni) bulk_g2s(st + L.oi_off, reinterpret_cast<const void *>(i0), ni, &bar[u & 1u]);
+  };
+
+  for (uint32_t g0 = R0; g0 < R1; g0 += kTileRows) {
+    const uint32_t g1 = min(R1, g0 + kTileRows), ng = g1 - g0;
+    __syncthreads();  // previous group's tiles fully consumed
+    for (uint32_t i = tid; i <= ng; i += kTileNT) rp_s[i] = load_index(a.rp, a.rp_bits, g0 + i);
+    __syncthreads();
+    for (uint32_t i = tid; i <= ng; i += kTileNT) ep_s[i] = ld_idx(op, rp_s[i]);
+    __syncthreads();
+    if (tid == 0) {  // greedy tiles of whole rows
+      uint32_t nt = 0, r = 0;
+      trow[0] = 0;
+      while (r < ng) {
+        uint32_t e = r + 1;
+        while (e < ng && ep_s[e + 1] - ep_s[r] <= kTileE && rp_s[e + 1] - rp_s[r] <= kTileS) ++e;
+        trow[++nt] = e;
+        r = e;
+      }
+      trow[kTileRows + 1] = nt;
+      for (uint32_t t = 0; t < 2 && t < nt; ++t) issue(trow[t], trow[t + 1], issued++);
+    }
+    if (!staged_x) {  // x is the only input produced by an earlier grid
+      pdl_wait();
+      const int kv = static_cast<int>(min64(a.k, kSmemValues));
+      for (int i = tid; i < kv; i += kTileNT) wv[i] = static_cast<float>(__ldg(a.omega + i) - a.bg);
+      const int64_t n4 = a.n >> 2;
+      if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+        const float4 *x4 = reinterpret_cast<const float4 *>(x);
+        float4 *xs4 = reinterpret_cast<float4 *>(xs);
+        for (int64_t i = tid; i < n4; i += kTileNT) xs4[i] = __ldg(x4 + i);
+        for (int64_t i = (n4 << 2) + tid; i < a.n; i += kTileNT) xs[i] = __ldg(x + i);
+      } else {
+        for (int64_t i = tid; i < a.n; i += kTileNT) xs[i] = __ldg(x + i);
+      }
+      y_empty = a.bg != 0.0 ? static_cast<float>(a.bg * a.colsum[0]) : 0.f;
+      staged_x = true;
+    }
+    __syncthreads();
+    const uint32_t nt = trow[kTileRows + 1];
+    for (uint32_t t = 0; t < nt; ++t) {
+      const uint32_t u = consumed++;
+      const uint32_t ta = trow[t], tb = trow[t + 1];
+      const uint32_t Sa = rp_s[ta], Ea = ep_s[ta], Eb = ep_s[tb];
+      mbar_wait(&bar[u & 1u], (u >> 1) & 1u);
+      const unsigned char *st = smem + L.stage + (u & 1u) * L.stage_bytes;
+      const uint32_t ebase = static_cast<uint32_t>(
+          ((reinterpret_cast<uintptr_t>(col + Ea) & ~uintptr_t(15)) - reinterpret_cast<uintptr_t>(col)) / sizeof(ColT));
+      const uint32_t sbase = static_cast<uint32_t>(
+          ((reinterpret_cast<uintptr_t>(op + Sa) & ~uintptr_t(15)) - reinterpret_cast<uintptr_t>(op)) / sizeof(PtrT));
+      const uint32_t ibase = CSER ? static_cast<uint32_t>(((reinterpret_cast<uintptr_t>(oi + static_cast<size_t>(Sa) * oib) &
+                                                             ~uintptr_t(15)) - reinterpret_cast<uintptr_t>(oi)) / oib)
+                                  : 0u;
+      const ColT *cst = reinterpret_cast<const ColT *>(st + L.col_off);
+      const PtrT *ost = reinterpret_cast<const PtrT *>(st + L.op_off);
+      const unsigned char *ist = st + L.oi_off;
+      // ---- (A) gather + per-thread prefix of this thread's 16 aligned entry slots
+      float run = 0.f;
+      {
+        const uint32_t q0 = tid * kTileEPT;  // aligned-relative slot
+        const uint32_t g0e = ebase + q0;      // global entry of slot q0
+        if (g0e < Eb) {
+          float o[kTileEPT];
+#pragma unroll
+          for (int v = 0; v < NVT; ++v) {
+            uint32_t c[CV::kPer];
+            CV::unpack(reinterpret_cast<const uint4 *>(cst)[tid * NVT + v], c);
+#pragma unroll
+            for (int i = 0; i < CV::kPer; ++i) {
+              const uint32_t ge = g0e + v * CV::kPer + i;
+              float g = 0.f;
+              if (ge >= Ea && ge < Eb) g = xs[c[i]];
+              run += g;
+              o[v * CV::kPer + i] = run;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kTileEPT / 4; ++q)
+            *reinterpret_cast<float4 *>(pre + q * (kTileNT * 4) + tid * 4) =
+                make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        }
+      }
+      // ---- (B) block scan of thread totals
+      float incl = run;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const float v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+      }
+      tinc[tid] = incl;
+      tex[tid] = incl - run;
+      if (lane == 31) winc[wid] = incl;  // warp total
+      __syncthreads();
+      if (wid == 0) {
+        const float wt = lane < kTileWarps ? winc[lane] : 0.f;
+        float wi = wt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const float v = __shfl_up_sync(0xffffffffu, wi, d);
+          if (lane >= d) wi += v;
+        }
+        if (lane < kTileWarps) wex[lane] = wi - wt;
+      }
+      __syncthreads();
+      // sum of aligned slots [lo, hi), lo < hi
+      auto range_sum = [&](uint32_t lo, uint32_t hi) -> float {
+        const uint32_t tl = lo / kTileEPT, th = (hi - 1) / kTileEPT;
+        const float pl = (lo % kTileEPT) ? pre[tpos(lo - 1)] : 0.f;
+        const float ph = pre[tpos(hi - 1)];
+        if (tl == th) return ph - pl;
+        const float tl_tot = tinc[tl] - tex[tl];
+        const uint32_t wl = tl >> 5, wh = th >> 5;
+        if (wl == wh) return ((tl_tot - pl) + (tex[th] - tinc[tl])) + ph;
+        const float mid = (wl + 1 < wh) ? (wex[wh] - wex[wl + 1]) : 0.f;  // whole warps in between
+        return (((tl_tot - pl) + (winc[wl] - tinc[tl])) + mid + tex[th]) + ph;
+      };
+      // ---- (C) warp per row: one lane per segment, one fma per segment
+      for (uint32_t r = ta + wid; r < tb; r += kTileWarps) {
+        const uint32_t s0 = rp_s[r], s1 = rp_s[r + 1];
+        float acc = 0.f;
+        for (uint32_t s = s0 + lane; s < s1; s += 32) {
+          const uint32_t stt = ost[s - sbase], enn = ost[s + 1 - sbase];
+          if (enn > stt) {
+            int k;
+            if (CSER) {
+              const uint32_t ii = s - ibase;
+              k = oib == 1 ? ist[ii] : (oib == 2 ? reinterpret_cast<const uint16_t *>(ist)[ii]
+                                                  : static_cast<int>(reinterpret_cast<const uint32_t *>(ist)[ii]));
+            } else {
+              k = static_cast<int>(s - s0 + 1);
+            }
+            acc = fmaf(wv[k], range_sum(stt - ebase, enn - ebase), acc);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0)
+          y[g0 + r] = s1 > s0 ? (a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + a.bg * a.colsum[0]) : acc)
+                              : y_empty;
+      }
+      __syncthreads();  // stage (u % 2), the prefix table and scans are free again
+      if (tid == 0 && t + 2 < nt) issue(trow[t + 2], trow[t + 3], issued++);
+    }
+  }
+}
+
+template <typename ColT, typename PtrT, bool CSER>
+int launch_matvec_tile(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
+  const TileSmem L = tile_layout(a.k, a.n, sizeof(ColT), sizeof(PtrT), CSER ? a.oi_bits / 8 : 1);
+  auto kern = k_matvec_tile<ColT, PtrT, CSER>;
+  CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total)));
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms(), a.m)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTileNT);
+  cfg.dynamicSmemBytes = L.total;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CERDOT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a, x, y));
+  return CERDOT_OK;
+}
+
 // Generic mat-vec for alphabets beyond the u16 slot table: warp per row, lanes over segments.
 template <typename ColT, typename PtrT, bool CSER>
 __global__ void __launch_bounds__(256) k_matvec_generic(DotArgs a, const float *__restrict__ x,
@@ -668,6 +969,17 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
     return CERDOT_OK;
   }
   if (batch == 1) {
+    // rows that fit a tile (known from the encoding's row statistics): CTA-tile TMA pipeline
+    const char *force_path = getenv("CERDOT_MATVEC_PATH");
+    const bool tile_ok = a.max_row_nnz > 0 && a.max_row_nnz <= kTileE && a.max_row_segs <= kTileS &&
+                         a.k <= kSmemValues &&
+                         tile_layout(a.k, a.n, sizeof(ColT), sizeof(PtrT), CSER ? a.oi_bits / 8 : 1).total <=
+                             static_cast<uint32_t>(kMaxSmemBytes);
+    // measured on B200: the tile pipeline wins when there are fewer rows than warps in the window kernel
+    // (ResNet conv 512 rows: 8.2 vs 13+ us); with >= 1 row per warp the window kernel wins (AlexNet, VGG)
+    const bool few_rows = a.m < int64_t(num_sms()) * 16;
+    const int want = force_path ? atoi(force_path) : (few_rows ? 2 : 1);
+    if (tile_ok && want == 2) return launch_matvec_tile<ColT, PtrT, CSER>(a, x, y, st);
     // 32 warps per SM when x and the per-warp tables fit, else 16 warps with three windows in flight
     const char *force = getenv("CERDOT_MATVEC_NT");
     const bool wide = force ? atoi(force) == 1024
@@ -731,6 +1043,8 @@ int dot(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, fl
   a.k = mat->k;
   a.bg = mat->background;
   a.segs = mat->segments;
+  a.max_row_nnz = mat->max_row_nnz;
+  a.max_row_segs = mat->max_row_segments;
   if (a.m == 0 || batch == 0) return CERDOT_OK;
   if (a.bg != 0.0) {
     if (workspace == nullptr || workspace_bytes < sizeof(double) * static_cast<size_t>(batch))

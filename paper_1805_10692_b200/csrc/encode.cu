@@ -52,6 +52,7 @@ struct Ctrl {
   int mode_index;            // CSER background position
   int pad;
   double background;         // omega[0]
+  unsigned long long max_stat[3];  // largest per-row nnz, CER segments, CSER segments
 };
 
 struct FastWs {
@@ -394,6 +395,13 @@ __global__ void __launch_bounds__(1024) k_scan_rows(int64_t m, FastWs ws) {
     for (int j = 0; j < 3; ++j) part[j][t] += v[j];
     __syncthreads();
   }
+  // largest per-row statistic (max over the same partition, then over threads)
+  {
+    uint64_t mx[3] = {0, 0, 0};
+    for (int64_t r = r0; r < r1; ++r)
+      for (int j = 0; j < 3; ++j) mx[j] = max(mx[j], static_cast<uint64_t>(ws.row_stat[j * m + r]));
+    for (int j = 0; j < 3; ++j) atomicMax(&ws.ctrl->max_stat[j], static_cast<unsigned long long>(mx[j]));
+  }
   uint64_t run[3];
   for (int j = 0; j < 3; ++j) run[j] = part[j][t] - s[j];
   for (int64_t r = r0; r < r1; ++r)
@@ -636,6 +644,11 @@ int encode_plan(const void *w, int dtype, int64_t m, int64_t n, int64_t ldw, int
   info->mode_index = ctrl.mode_index;
   info->background = ctrl.background;
   info->path = 0;
+  CERDOT_CUDA_CHECK(cudaMemcpyAsync(&ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  CERDOT_CUDA_CHECK(cudaStreamSynchronize(st));
+  info->max_row_nnz = static_cast<int64_t>(ctrl.max_stat[0]);
+  info->max_row_segments_cer = static_cast<int64_t>(ctrl.max_stat[1]);
+  info->max_row_segments_cser = static_cast<int64_t>(ctrl.max_stat[2]);
   return CERDOT_OK;
 }
 

@@ -71,6 +71,8 @@ class DeviceEncoding:
     bits: dict  # name -> 8/16/32 for colI, omegaPtr, rowPtr, omegaI
     arena: object  # torch.uint8 cuda tensor
     offsets: dict  # name -> byte offset
+    max_row_nnz: int = 0  # largest row in entries (0 = unknown)
+    max_row_segments: int = 0  # largest row in segments (0 = unknown)
     _struct: object = field(default=None, repr=False)
 
     @staticmethod
@@ -120,6 +122,8 @@ class DeviceEncoding:
             s.row_ptr_bits = self.bits["rowPtr"]
             s.omega_index_bits = self.bits.get("omegaI", 8)
             s.background = self.background
+            s.max_row_nnz = self.max_row_nnz
+            s.max_row_segments = self.max_row_segments
             self._struct = s
         return self._struct
 
@@ -163,5 +167,10 @@ class DeviceEncoding:
         arena = staging.to(dev, non_blocking=True)
         torch.cuda.current_stream(dev).synchronize()
         bg = float(omega[mode_index] if kind == _native.CSER else omega[0]) if k else 0.0
-        return cls(kind, m, n, k, nnz, segs, mode_index, bg, bits, arena, offsets)
+        rp = host["rowPtr"].astype(np.int64)
+        optr = host["omegaPtr"].astype(np.int64)
+        seg_rows = np.diff(rp) if m else np.zeros(0, dtype=np.int64)
+        nnz_rows = (optr[rp[1:]] - optr[rp[:-1]]) if m else np.zeros(0, dtype=np.int64)
+        return cls(kind, m, n, k, nnz, segs, mode_index, bg, bits, arena, offsets,
+                   int(nnz_rows.max()) if nnz_rows.size else 0, int(seg_rows.max()) if seg_rows.size else 0)
 

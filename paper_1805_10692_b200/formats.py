@@ -261,7 +261,8 @@ def _encode(a, kind: int, index_bits, background):
         offsets, total = DeviceEncoding.layout(kind, m, info.k, info.nnz, segs, bits)
         arena = torch.empty(total, dtype=torch.uint8, device=w.device)
         dev = DeviceEncoding(kind, m, n, info.k, info.nnz, segs, info.mode_index if kind == _native.CSER else 0,
-                             0.0, bits, arena, offsets)
+                             0.0, bits, arena, offsets, int(info.max_row_nnz),
+                             int(info.max_row_segments_cser if kind == _native.CSER else info.max_row_segments_cer))
         _native.check(L.cerdot_encode_fill(info, kind, ws.data_ptr(), ws_bytes, dev.ptr("omega"), dev.ptr("colI"),
                                            bits["colI"], dev.ptr("omegaPtr"), bits["omegaPtr"], dev.ptr("rowPtr"),
                                            bits["rowPtr"], dev.ptr("omegaI") if kind == _native.CSER else None,

@@ -223,3 +223,34 @@ def test_wide_alphabets_up_to_fast_limit():
         assert digest(enc.omega_ptr) == digest(ref["omegaPtr"])
         assert digest(enc.row_ptr) == digest(ref["rowPtr"])
         assert np.array_equal(cd.dot(enc, x), w @ x)
+
+
+@pytest.mark.parametrize("path", ["tile", "window"])
+@pytest.mark.parametrize("name", ["oracle", "alexnet-fc6", "resnet-conv"])
+def test_matvec_paths_agree_with_oracle(monkeypatch, config_goldens, name, path):
+    """Both mat-vec kernels (CTA-tile TMA pipeline and the warp-window kernel) meet the bar."""
+    monkeypatch.setenv("CERDOT_MATVEC_PATH", "1" if path == "window" else "2")
+    meta, ys = config_goldens
+    w, _ = synth.make_layer(name)
+    x1 = np.random.default_rng(1).standard_normal(w.shape[1], dtype=np.float32)
+    wt = torch.from_numpy(w).cuda()
+    for kind in ("cer", "cser"):
+        enc = (cd.encode_cer if kind == "cer" else cd.encode_cser)(wt)
+        assert rel_err(cd.dot(enc, x1), ys[f"{name}/{kind}/b1"]) <= REL_TOL, (name, kind, path)
+
+
+@pytest.mark.parametrize("path", ["1", "2"])
+def test_matvec_tile_edge_rows(monkeypatch, path):
+    """Empty rows, single-entry rows, a long row next to short ones, non-zero background (both kernels)."""
+    monkeypatch.setenv("CERDOT_MATVEC_PATH", path)
+    rng = np.random.default_rng(9)
+    w = np.zeros((300, 700))
+    w[5, :] = rng.integers(1, 4, size=700)           # a dense row (700 entries, few segments)
+    w[7, 3] = 2.0                                     # single entry
+    w[100:300:3, ::5] = rng.integers(-3, 4, size=(67, 140))
+    x = rng.integers(-4, 5, size=700).astype(np.float64)
+    for bg in (None, 1.0):
+        for encode in (cd.encode_cer, cd.encode_cser):
+            enc = encode(w, background=bg)
+            y = cd.dot(enc, x)
+            assert np.array_equal(y, w @ x), (encode.__name__, bg)
