@@ -812,13 +812,14 @@ __device__ __forceinline__ XVec<V> ld_x(const float *p, int64_t cb, int64_t batc
   return r;
 }
 
-// Mat-mat: warp per (row, 32*V columns of the batch).
+// Mat-mat: warp per (row, 32*V batch columns).  The row's colI entries are walked as one
+// contiguous stream (32-entry chunks loaded lane-parallel, the next chunk prefetched); segments are
+// iterated at warp level (bounds and omegaI loaded 32 at a time), so an entry costs one shuffle, one
+// V-wide vector load of its X row and V adds, eight loads in flight; one fma per segment per column.
 template <typename ColT, typename PtrT, bool CSER, int V>
-__global__ void __launch_bounds__(256) k_matmat(DotArgs a, const float *__restrict__ x, int64_t ldx, int64_t batch,
+__global__ void __launch_bounds__(256, (V == 4 ? 4 : 1)) k_matmat(DotArgs a, const float *__restrict__ x, int64_t ldx, int64_t batch,
                                                 float *__restrict__ y, int64_t ldy) {
-  __shared__ int slot_all[8][32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int *slots = slot_all[wid];
+  const int lane = threadIdx.x & 31;
   const ColT *col = static_cast<const ColT *>(a.col);
   const PtrT *op = static_cast<const PtrT *>(a.op);
   const int64_t chunks = ceil_div(batch, 32 * V);
@@ -826,75 +827,89 @@ __global__ void __launch_bounds__(256) k_matmat(DotArgs a, const float *__restri
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t u = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < units; u += nwarps) {
     const int64_t row = u / chunks, cb = (u - row * chunks) * 32 * V + lane * V;
-    const int64_t s0 = load_index(a.rp, a.rp_bits, row), s1 = load_index(a.rp, a.rp_bits, row + 1);
-    float acc[V], sum[V];
+    const uint32_t s0 = load_index(a.rp, a.rp_bits, row), s1 = load_index(a.rp, a.rp_bits, row + 1);
+    float acc[V];
 #pragma unroll
-    for (int j = 0; j < V; ++j) acc[j] = sum[j] = 0.f;
-    int cur_k = -1;
+    for (int q = 0; q < V; ++q) acc[q] = 0.f;
     if (s1 > s0) {
-      const int64_t e0 = ld_idx(op, s0), e1 = ld_idx(op, s1);
-      int64_t sc = s0;
-      const float *xb = x + cb;
-      for (int64_t base = e0; base < e1; base += 32) {
-        const int64_t wn = base + 32;
-        slots[lane] = -1;
-        __syncwarp();
-        for (;;) {
-          const int64_t s = sc + lane;
-          const bool in_row = s < s1;
-          const int64_t st = in_row ? static_cast<int64_t>(ld_idx(op, s)) : INT64_MAX;
-          const int64_t en = in_row ? static_cast<int64_t>(ld_idx(op, s + 1)) : INT64_MAX;
-          const bool here = st < wn;
-          if (here && en > st)
-            slots[st - base] = CSER ? static_cast<int>(load_index(a.oi, a.oi_bits, s)) : static_cast<int>(s - s0 + 1);
-          const int cnt = __popc(__ballot_sync(0xffffffffu, here));
-          sc += cnt;
-          if (cnt < 32) break;
-        }
-        __syncwarp();
-        const int ne = static_cast<int>(min64(32, e1 - base));
-        const uint32_t my_col = lane < ne ? ld_idx(col, base + lane) : 0u;
-        const int my_k = slots[lane];
-        for (int j0 = 0; j0 < ne; j0 += 8) {
-          XVec<V> xv[8];
+      const float *xb = x + cb;                       // this lane's columns
+      const bool full = cb + V <= batch;              // lanes past the batch end take the guarded path
+      const int nval = static_cast<int>(max64(0, min64(V, batch - cb)));
+      const uint32_t ldx32 = static_cast<uint32_t>(ldx);
+      const uint32_t e0 = ld_idx(op, s0), e1 = ld_idx(op, s1);
+      // colI stream: cur holds entries [ch, ch + 32), nxt the following 32
+      uint32_t ch = e0;
+      uint32_t cur = (ch + lane < e1) ? ld_idx(col, ch + lane) : 0u;
+      uint32_t nxt = (ch + 32 + lane < e1) ? ld_idx(col, ch + 32 + lane) : 0u;
+      for (uint32_t sb = s0; sb < s1; sb += 32) {
+        // bounds / element of segments sb .. sb+31 (lane l: segment sb + l)
+        const uint32_t my_s = sb + lane;
+        const uint32_t my_st = my_s < s1 ? ld_idx(op, my_s) : 0u;
+        const uint32_t my_en = my_s < s1 ? ld_idx(op, my_s + 1) : 0u;
+        int my_k = 0;
+        if (my_s < s1) my_k = CSER ? static_cast<int>(load_index(a.oi, a.oi_bits, my_s)) : static_cast<int>(my_s - s0 + 1);
+        const float my_v = my_s < s1 ? static_cast<float>(__ldg(a.omega + my_k) - a.bg) : 0.f;
+        const int nseg = static_cast<int>(min64(32, s1 - sb));
+        for (int t = 0; t < nseg; ++t) {
+          uint32_t e = __shfl_sync(0xffffffffu, my_st, t);
+          const uint32_t en = __shfl_sync(0xffffffffu, my_en, t);
+          if (en <= e) continue;
+          float sum[V];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const uint32_t c = __shfl_sync(0xffffffffu, my_col, j0 + t);
-            if (j0 + t < ne) xv[t] = ld_x<V>(xb + static_cast<int64_t>(c) * ldx, cb, batch);
-          }
+          for (int q = 0; q < V; ++q) sum[q] = 0.f;
+          while (e < en) {
+            uint32_t j = e - ch;
+            if (j >= 32u) {  // advance the colI stream
+              ch += 32;
+              cur = nxt;
+              nxt = (ch + 32 + lane < e1) ? ld_idx(col, ch + 32 + lane) : 0u;
+              continue;
+            }
+            const uint32_t here = min(en - e, 32u - j);
+            for (uint32_t t0 = 0; t0 < here; t0 += 8) {
+              XVec<V> xv[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const int k = __shfl_sync(0xffffffffu, my_k, j0 + t);
-            if (j0 + t < ne) {
-              if (k >= 0) {
-                if (cur_k >= 0) {
-                  const float sv = cur_k < 0 ? 0.f : static_cast<float>(__ldg(a.omega + cur_k) - a.bg);
+              for (int i = 0; i < 8; ++i) {
+                const uint32_t c = __shfl_sync(0xffffffffu, cur, (j + t0 + i) & 31u);
+                if (t0 + i < here) {
+                  const float *p = xb + static_cast<size_t>(c) * ldx32;
+                  if (full) {
+                    if (V == 4) {
+                      const float4 t4 = __ldg(reinterpret_cast<const float4 *>(p));
+                      xv[i].v[0] = t4.x; xv[i].v[1] = t4.y; xv[i].v[2] = t4.z; xv[i].v[V - 1] = t4.w;
+                    } else if (V == 2) {
+                      const float2 t2 = __ldg(reinterpret_cast<const float2 *>(p));
+                      xv[i].v[0] = t2.x; xv[i].v[V - 1] = t2.y;
+                    } else {
+                      xv[i].v[0] = __ldg(p);
+                    }
+                  } else {
 #pragma unroll
-                  for (int q = 0; q < V; ++q) acc[q] = fmaf(sv, sum[q], acc[q]);
+                    for (int q = 0; q < V; ++q) xv[i].v[q] = q < nval ? __ldg(p + q) : 0.f;
+                  }
                 }
-#pragma unroll
-                for (int q = 0; q < V; ++q) sum[q] = 0.f;
-                cur_k = k;
               }
 #pragma unroll
-              for (int q = 0; q < V; ++q) sum[q] += xv[t].v[q];
-            }
-          }
-        }
-        __syncwarp();
-      }
-      if (cur_k >= 0) {
-        const float sv = static_cast<float>(__ldg(a.omega + cur_k) - a.bg);
+              for (int i = 0; i < 8; ++i)
+                if (t0 + i < here) {
 #pragma unroll
-        for (int q = 0; q < V; ++q) acc[q] = fmaf(sv, sum[q], acc[q]);
+                  for (int q = 0; q < V; ++q) sum[q] += xv[i].v[q];
+                }
+            }
+            e += here;
+          }
+          const float v = __shfl_sync(0xffffffffu, my_v, t);
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] = fmaf(v, sum[q], acc[q]);
+        }
       }
     }
     float *yr = y + row * ldy;
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const int64_t c = cb + j;
+    for (int q = 0; q < V; ++q) {
+      const int64_t c = cb + q;
       if (c < batch)
-        yr[c] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc[j]) + a.bg * a.colsum[c]) : acc[j];
+        yr[c] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc[q]) + a.bg * a.colsum[c]) : acc[q];
     }
   }
 }
