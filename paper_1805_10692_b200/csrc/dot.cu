@@ -48,6 +48,7 @@ constexpr int kMatvecThreads = 512;
 constexpr int kMatvecWarps = kMatvecThreads / 32;
 constexpr int kSmemValues = 4096;             // omega entries cached in smem
 constexpr int kMaxSmemBytes = 227 * 1024;
+constexpr size_t kHalfSmemBytes = 112 * 1024;  // two CTAs per SM (228 KB minus 1 KB reserved each)
 
 struct DotArgs {
   const double *omega;
@@ -182,7 +183,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 struct MatvecSmem {
   uint32_t wv, pre, off, ring_op, ring_oi, xs, total;
 };
-__host__ __device__ __forceinline__ MatvecSmem matvec_layout(int64_t k, int64_t n_smem, uint32_t warps) {
+__host__ __device__ __forceinline__ MatvecSmem matvec_layout(int64_t k, int64_t n_smem, uint32_t warps, uint32_t depth,
+                                                             uint32_t oi_bytes) {
   MatvecSmem L{};
   uint32_t o = 0;
   auto take = [&](uint32_t bytes) {
@@ -193,29 +195,29 @@ __host__ __device__ __forceinline__ MatvecSmem matvec_layout(int64_t k, int64_t 
   L.wv = take(static_cast<uint32_t>(min64(k, kSmemValues)) * 4u);
   L.pre = take(warps * kWin * 4u);
   L.off = take(warps * 32u * 4u);
-  L.ring_op = take(warps * kFifoDepth * 128u);
-  L.ring_oi = take(warps * kFifoDepth * 128u);
+  L.ring_op = take(warps * depth * 128u);
+  L.ring_oi = take(warps * depth * 32u * oi_bytes);
   L.xs = take(static_cast<uint32_t>(n_smem) * 4u);
   L.total = o;
   return L;
 }
 
-template <typename ColT, typename PtrT, bool CSER, bool XSMEM, int NT, int NBUF>
-__global__ void __launch_bounds__(NT, 1) k_matvec(DotArgs a, const float *__restrict__ x, float *__restrict__ y) {
+template <typename ColT, typename PtrT, bool CSER, bool XSMEM, int NT, int NBUF, int MINB, int D>
+__global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__restrict__ x, float *__restrict__ y) {
   constexpr int kWarps = NT / 32;
   using CV = ColVec<ColT>;
   constexpr uint32_t W = kWin;
   constexpr int NV = kEPL / CV::kPer;
   constexpr uint32_t kAlign = CV::kPer;
-  constexpr int D = kFifoDepth;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  MatvecSmem L = matvec_layout(a.k, XSMEM ? a.n : 0, kWarps);
+  const uint32_t oib = CSER ? static_cast<uint32_t>(a.oi_bits / 8) : 1u;
+  MatvecSmem L = matvec_layout(a.k, XSMEM ? a.n : 0, kWarps, D, oib);
   float *wv = reinterpret_cast<float *>(smem + L.wv);
   float *pre = reinterpret_cast<float *>(smem + L.pre) + wid * W;
   float *off = reinterpret_cast<float *>(smem + L.off) + wid * 32;
   unsigned char *ring_op = smem + L.ring_op + wid * D * 128;
-  unsigned char *ring_oi = smem + L.ring_oi + wid * D * 128;
+  unsigned char *ring_oi = smem + L.ring_oi + wid * D * 32 * oib;
   float *xs = reinterpret_cast<float *>(smem + L.xs);
   const ColT *col = static_cast<const ColT *>(a.col);
   const PtrT *op = static_cast<const PtrT *>(a.op);
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(NT, 1) k_matvec(DotArgs a, const float *__rest
       if (static_cast<uint32_t>(lane) < nch) {
         const uint32_t e = base + lane * per_oi;
         if (e < static_cast<uint32_t>(a.segs) && base < s_end)
-          cp_async4(ring_oi + slot * 128 + lane * 4, static_cast<const unsigned char *>(a.oi) + e * ob_bytes);
+          cp_async4(ring_oi + slot * 32 * ob_bytes + lane * 4, static_cast<const unsigned char *>(a.oi) + e * ob_bytes);
       }
     }
     cp_async_commit();
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(NT, 1) k_matvec(DotArgs a, const float *__rest
   };
   auto ring_oi_val = [&](uint32_t s) -> int {
     const uint32_t r = (s - fb) % (32u * D);
-    const unsigned char *slot = ring_oi + (r >> 5) * 128;
+    const unsigned char *slot = ring_oi + (r >> 5) * 32u * oib;
     switch (a.oi_bits) {
       case 8: return slot[r & 31u];
       case 16: return reinterpret_cast<const uint16_t *>(slot)[r & 31u];
@@ -401,6 +403,30 @@ __global__ void __launch_bounds__(NT, 1) k_matvec(DotArgs a, const float *__rest
     }
     const float excl = __shfl_up_sync(0xffffffffu, incl, 1);
     off[lane] = lane ? excl : 0.f;
+    if (w.w0 == (w.e0 & ~(kAlign - 1)) && wn >= w.e1) {
+      // ---- the whole row is in this window: its segments are independent (no carry, no ring)
+      __syncwarp();
+      const PtrT *opp = op;
+#pragma unroll 4
+      for (uint32_t s = w.s0 + lane; s < w.s1; s += 32) {
+        const uint32_t st = __ldg(opp + s), en = __ldg(opp + s + 1);
+        if (en > st) {
+          const int k = CSER ? static_cast<int>(load_index(a.oi, a.oi_bits, s)) : static_cast<int>(s - w.s0 + 1);
+          const uint32_t lo = st - w0, b = en - 1u - w0;
+          const float pb = pre[ppos(b)];
+          float total;
+          if (lo == 0u) {
+            total = off[b >> 5] + pb;
+          } else {
+            const uint32_t a0 = lo - 1u;
+            const float pa = pre[ppos(a0)];
+            total = ((a0 >> 5) == (b >> 5)) ? pb - pa : (off[b >> 5] + pb) - (off[a0 >> 5] + pa);
+          }
+          acc = fmaf(wv[k], total, acc);
+        }
+      }
+      sc = w.s1;
+    } else
     // ---- segments overlapping this window: one lane per segment
     for (;;) {
       cp_async_wait<D - 2>();  // batches ft and ft+1 hold segments [sc, sc + 32]
@@ -950,14 +976,15 @@ __global__ void __launch_bounds__(1024) k_vecsum(const float *__restrict__ x, in
   }
 }
 
-size_t matvec_smem(int64_t k, int64_t n, bool xsmem, uint32_t warps) {
-  return matvec_layout(k, xsmem ? n : 0, warps).total;
+size_t matvec_smem(int64_t k, int64_t n, bool xsmem, uint32_t warps, uint32_t depth, uint32_t oib) {
+  return matvec_layout(k, xsmem ? n : 0, warps, depth, oib).total;
 }
 
-template <typename ColT, typename PtrT, bool CSER, bool XSMEM, int NT, int NBUF>
+template <typename ColT, typename PtrT, bool CSER, bool XSMEM, int NT, int NBUF, int MINB, int D>
 int launch_matvec(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
-  const size_t smem = matvec_smem(a.k, a.n, XSMEM, NT / 32);
-  auto kern = k_matvec<ColT, PtrT, CSER, XSMEM, NT, NBUF>;
+  const uint32_t oib = CSER ? static_cast<uint32_t>(a.oi_bits / 8) : 1u;
+  const size_t smem = matvec_smem(a.k, a.n, XSMEM, NT / 32, D, oib);
+  auto kern = k_matvec<ColT, PtrT, CSER, XSMEM, NT, NBUF, MINB, D>;
   CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   // every SM gets a CTA; rows are split fractionally over all warps (R0 = gw*m/warps)
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms(), a.m)));
@@ -995,14 +1022,21 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
     const bool few_rows = a.m < int64_t(num_sms()) * 16;
     const int want = force_path ? atoi(force_path) : (few_rows ? 2 : 1);
     if (tile_ok && want == 2) return launch_matvec_tile<ColT, PtrT, CSER>(a, x, y, st);
-    // 32 warps per SM when x and the per-warp tables fit, else 16 warps with three windows in flight
+    // Prefer the co-resident variant (16 warps, <= 64 regs, <= half the SM's shared memory): two
+    // consecutive calls' CTAs then share an SM and, with programmatic dependent launch, the next call's
+    // index prologue (rowPtr -> omegaPtr -> colI latency chain) overlaps this call's work.
+    const uint32_t oib = CSER ? static_cast<uint32_t>(a.oi_bits / 8) : 1u;
+    // (measured: AlexNet-fc6 12.5 us co-resident vs 10.6 us exclusive -- the post-wait chain dominates,
+    // so the co-resident variant is opt-in: CERDOT_MATVEC_NT=1)
     const char *force = getenv("CERDOT_MATVEC_NT");
-    const bool wide = force ? atoi(force) == 1024
-                            : matvec_smem(a.k, a.n, true, 32) <= static_cast<size_t>(kMaxSmemBytes);
-    if (wide) return launch_matvec<ColT, PtrT, CSER, true, 1024, 1>(a, x, y, st);
-    const bool xsmem = matvec_smem(a.k, a.n, true, 16) <= static_cast<size_t>(kMaxSmemBytes);
-    return xsmem ? launch_matvec<ColT, PtrT, CSER, true, 512, 3>(a, x, y, st)
-                 : launch_matvec<ColT, PtrT, CSER, false, 512, 3>(a, x, y, st);
+    const int want_nt = force ? atoi(force) : 0;
+    if (want_nt == 1 && matvec_smem(a.k, a.n, true, 16, 3, oib) <= kHalfSmemBytes)
+      return launch_matvec<ColT, PtrT, CSER, true, 512, 1, 2, 3>(a, x, y, st);
+    const bool wide = want_nt == 1024 || (want_nt == 0 && matvec_smem(a.k, a.n, true, 32, 4, oib) <= kMaxSmemBytes);
+    if (wide) return launch_matvec<ColT, PtrT, CSER, true, 1024, 1, 1, 4>(a, x, y, st);
+    const bool xsmem = matvec_smem(a.k, a.n, true, 16, 4, oib) <= static_cast<size_t>(kMaxSmemBytes);
+    return xsmem ? launch_matvec<ColT, PtrT, CSER, true, 512, 3, 1, 4>(a, x, y, st)
+                 : launch_matvec<ColT, PtrT, CSER, false, 512, 3, 1, 4>(a, x, y, st);
   }
   const bool al4 = (ldx % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
   const bool al2 = (ldx % 2 == 0) && (reinterpret_cast<uintptr_t>(x) % 8 == 0);
