@@ -35,6 +35,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <string>
 
 #include "common.cuh"
@@ -63,6 +66,24 @@ struct DotArgs {
   int64_t segs;          // segment count (omegaPtr has segs + 1 entries)
   int64_t max_row_nnz, max_row_segs;
 };
+
+// Raise a kernel's dynamic shared-memory limit once per kernel (and device) -- the host call costs ~us.
+template <typename K>
+int allow_max_smem(K kern) {
+  static std::mutex mu;
+  static std::set<std::pair<const void *, int>> done;
+  int dev = 0;
+  CERDOT_CUDA_CHECK(cudaGetDevice(&dev));
+  const auto key = std::make_pair(reinterpret_cast<const void *>(kern), dev);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(key)) return CERDOT_OK;
+  }
+  CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  std::lock_guard<std::mutex> lock(mu);
+  done.insert(key);
+  return CERDOT_OK;
+}
 
 template <typename T>
 __device__ __forceinline__ uint32_t ld_idx(const T *p, int64_t i) {
@@ -775,7 +796,7 @@ template <typename ColT, typename PtrT, bool CSER>
 int launch_matvec_tile(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
   const TileSmem L = tile_layout(a.k, a.n, sizeof(ColT), sizeof(PtrT), CSER ? a.oi_bits / 8 : 1);
   auto kern = k_matvec_tile<ColT, PtrT, CSER>;
-  CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total)));
+  if (int rc_ = allow_max_smem(kern)) return rc_;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms(), a.m)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -985,7 +1006,7 @@ int launch_matvec(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
   const uint32_t oib = CSER ? static_cast<uint32_t>(a.oi_bits / 8) : 1u;
   const size_t smem = matvec_smem(a.k, a.n, XSMEM, NT / 32, D, oib);
   auto kern = k_matvec<ColT, PtrT, CSER, XSMEM, NT, NBUF, MINB, D>;
-  CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (int rc_ = allow_max_smem(kern)) return rc_;
   // every SM gets a CTA; rows are split fractionally over all warps (R0 = gw*m/warps)
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms(), a.m)));
   cudaLaunchConfig_t cfg = {};

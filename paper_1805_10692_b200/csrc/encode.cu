@@ -20,8 +20,8 @@
 //                   columns into colI: (row, rank, col) order without a sort
 //                                                         (formats.py:220-221, 241-247, 273-283)
 //
-// Alphabets larger than CERDOT_FAST_K take CERDOT_E_UNSUPPORTED for now
-// (reported back as RuntimeError by the Python layer).
+// Alphabets larger than CERDOT_FAST_K take the sort-based path in encode_sort.cu (the plan then asks
+// for a larger workspace with CERDOT_E_WORKSPACE).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -615,9 +615,8 @@ int encode_plan(const void *w, int dtype, int64_t m, int64_t n, int64_t ldw, int
   Ctrl ctrl{};
   CERDOT_CUDA_CHECK(cudaMemcpyAsync(&ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
   CERDOT_CUDA_CHECK(cudaStreamSynchronize(st));
-  if (ctrl.overflow)
-    return fail(CERDOT_E_UNSUPPORTED, "alphabet has more than " + std::to_string(kFastDistinct) +
-                                          " distinct values: the sort-based conversion path is not built yet");
+  if (ctrl.overflow)  // alphabet too large for the on-chip tables: sort-based path (encode_sort.cu)
+    return encode_sort_plan(w, dtype, m, n, ldw, bg_mode, bg_value, workspace, workspace_bytes, info, st);
   k_alphabet<<<1, 1024, 0, st>>>(ws, bg_mode, bg_value);
   CERDOT_LAUNCH_CHECK();
   CERDOT_CUDA_CHECK(cudaMemcpyAsync(&ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
@@ -656,6 +655,9 @@ int encode_fill(const cerdot_encode_info *info, int kind, void *workspace, size_
                 void *col, int col_bits, void *op, int op_bits, void *rp, int rp_bits, void *oi, int oi_bits,
                 cudaStream_t st) {
   const int64_t m = info->m, n = info->n;
+  if (info->path == 1)
+    return encode_sort_fill(info, kind, workspace, workspace_bytes, omega, col, col_bits, op, op_bits, rp, rp_bits, oi,
+                            oi_bits, st);
   if (workspace == nullptr || workspace_bytes < encode_workspace_bytes(m, n))
     return fail(CERDOT_E_WORKSPACE, "encode workspace too small");
   FastWs ws = carve(workspace, m, n);

@@ -14,6 +14,13 @@ int encode_fill(const cerdot_encode_info *info, int kind, void *workspace, size_
                 void *col, int col_bits, void *op, int op_bits, void *rp, int rp_bits, void *oi, int oi_bits,
                 cudaStream_t st);
 
+size_t encode_sort_workspace_bytes(int64_t m, int64_t n);
+int encode_sort_plan(const void *w, int dtype, int64_t m, int64_t n, int64_t ldw, int bg_mode, double bg_value,
+                     void *workspace, size_t workspace_bytes, cerdot_encode_info *info, cudaStream_t st);
+int encode_sort_fill(const cerdot_encode_info *info, int kind, void *workspace, size_t workspace_bytes, double *omega,
+                     void *col, int col_bits, void *op, int op_bits, void *rp, int rp_bits, void *oi, int oi_bits,
+                     cudaStream_t st);
+
 int dot(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy, void *workspace,
         size_t workspace_bytes, cudaStream_t st);
 

@@ -250,8 +250,15 @@ def _encode(a, kind: int, index_bits, background):
     bg_value = 0.0 if background is None else float(background)
     with torch.cuda.device(w.device):
         st = stream_ptr(w.device)
-        _native.check(L.cerdot_encode_plan(w.data_ptr() if w.numel() else None, dtype, m, n, n, bg_mode, bg_value,
-                                           ws.data_ptr(), ws_bytes, info, st))
+        rc = L.cerdot_encode_plan(w.data_ptr() if w.numel() else None, dtype, m, n, n, bg_mode, bg_value,
+                                  ws.data_ptr(), ws_bytes, info, st)
+        if rc == _native.E_WORKSPACE and info.workspace_bytes > ws_bytes:
+            # large alphabet: the sort-based conversion needs more scratch; plan again with it
+            ws_bytes = info.workspace_bytes
+            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=w.device)
+            rc = L.cerdot_encode_plan(w.data_ptr(), dtype, m, n, n, bg_mode, bg_value, ws.data_ptr(), ws_bytes, info,
+                                      st)
+        _native.check(rc)
         segs = info.segments_cser if kind == _native.CSER else info.segments_cer
         bits = {"colI": _resolve_bits(max(n - 1, 0), index_bits)}
         if kind == _native.CSER:

@@ -254,3 +254,28 @@ def test_matvec_tile_edge_rows(monkeypatch, path):
             enc = encode(w, background=bg)
             y = cd.dot(enc, x)
             assert np.array_equal(y, w @ x), (encode.__name__, bg)
+
+
+@pytest.mark.parametrize("shape,distinct", [((64, 300), None), ((40, 120), 2100), ((7, 5000), 3000)])
+def test_sort_path_large_alphabets(shape, distinct):
+    """Alphabets beyond the on-chip tables take the sort-based conversion: still bit-exact."""
+    rng = np.random.default_rng(sum(shape))
+    if distinct is None:  # every value distinct (quantised-free real matrix)
+        w = rng.normal(size=shape)
+    else:
+        w = rng.choice(rng.normal(size=distinct), size=shape)
+        w[rng.random(shape) < 0.3] = 0.0
+    x = rng.normal(size=shape[1])
+    for bg in (None, 0.0, 12.5):
+        for encode, ref_encode in ((cd.encode_cer, numpy_port.encode_cer), (cd.encode_cser, numpy_port.encode_cser)):
+            enc = encode(w, background=bg)
+            ref = ref_encode(w, background=bg)
+            tag = (shape, distinct, bg, encode.__name__)
+            assert np.array_equal(enc.omega, ref["omega"]), tag
+            assert np.array_equal(enc.col_index, ref["colI"]) and enc.col_index.dtype == ref["colI"].dtype, tag
+            assert np.array_equal(enc.omega_ptr, ref["omegaPtr"]) and enc.omega_ptr.dtype == ref["omegaPtr"].dtype, tag
+            assert np.array_equal(enc.row_ptr, ref["rowPtr"]) and enc.row_ptr.dtype == ref["rowPtr"].dtype, tag
+            if encode is cd.encode_cser:
+                assert np.array_equal(enc.omega_index, ref["omegaI"]), tag
+                assert enc.mode_index == ref["mode_index"], tag
+            assert rel_err(cd.dot(enc, x), numpy_port.dot(ref, x)) <= REL_TOL, tag
