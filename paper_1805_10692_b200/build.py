@@ -21,7 +21,7 @@ HEADERS = ["common.cuh", "encode.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-         "-Xptxas", "-warn-spills"]
+         "-Xptxas", "-warn-spills"] + os.environ.get("NVCC_EXTRA", "").split()
 
 
 def _stale() -> bool:

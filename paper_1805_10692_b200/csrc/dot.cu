@@ -65,6 +65,7 @@ struct DotArgs {
   const double *colsum;  // batch doubles when bg != 0
   int64_t segs;          // segment count (omegaPtr has segs + 1 entries)
   int64_t max_row_nnz, max_row_segs;
+  int dbg;  // CERDOT_TRACE: print per-CTA phase timestamps (debug only)
 };
 
 // Raise a kernel's dynamic shared-memory limit once per kernel (and device) -- the host call costs ~us.
@@ -135,6 +136,12 @@ __device__ __forceinline__ uint4 ld_stream(const void *p) {
 // TMA-engine prefetch of a contiguous global range into L2 (no registers, no smem).
 __device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -247,6 +254,13 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kWarps + wid;
   const uint32_t R0 = static_cast<uint32_t>(gw * m / nw_total), R1 = static_cast<uint32_t>((gw + 1) * m / nw_total);
   pdl_launch_dependents();  // the next grid may start its own index prologue as our CTAs retire
+#ifdef CERDOT_TRACE_KERNELS
+  unsigned long long tr[7] = {gtimer(), 0, 0, 0, 0, 0, 0};
+#define CERDOT_TR(i, dep) \
+  if (a.dbg && tr[i] == 0) tr[i] = gtimer() + (dep)
+#else
+#define CERDOT_TR(i, dep)
+#endif
 
   // ------------------------------------------------------------ row groups (31 rows per lane-register group)
   uint32_t gG = R0, g_rp = 0, g_ep = 0;
@@ -376,9 +390,11 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
     gen(mb, B);
     gen(mc, C);
   }
+  CERDOT_TR(1, A[0].x & 0u);  // forces the prologue loads to complete for the timestamp
 
   // ------------------------------------------------------------ wait for the producer of x
   pdl_wait();
+  CERDOT_TR(2, 0u);
   const int kv = static_cast<int>(min64(a.k, kSmemValues));
   for (int i = threadIdx.x; i < kv; i += blockDim.x) wv[i] = static_cast<float>(__ldg(a.omega + i) - a.bg);
   if (XSMEM) {
@@ -393,6 +409,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
     }
   }
   __syncthreads();
+  CERDOT_TR(3, 0u);
   const float y_empty = a.bg != 0.0 ? static_cast<float>(a.bg * a.colsum[0]) : 0.f;
 
   // ------------------------------------------------------------ consumer
@@ -413,6 +430,23 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
     }
     const uint32_t w0 = w.w0, wn = w0 + W;
     stream_prefetch(w0, fb + 32u * ft);
+    // whole row in this window: issue its first 128 segment bounds (and omegaI) now, so the loads are
+    // in flight during the gather below (they do not depend on x)
+    const bool single = w.w0 == (w.e0 & ~(kAlign - 1)) && wn >= w.e1;
+    constexpr int kPre = NBUF > 1 ? 1 : 4;  // register budget: the 3-buffer variant keeps one prefetch batch
+    uint32_t pst[kPre], pen[kPre];
+    int pk[kPre];
+    if (single) {
+#pragma unroll
+      for (int i = 0; i < kPre; ++i) {
+        const uint32_t sidx = w.s0 + lane + 32u * i;
+        pst[i] = sidx < w.s1 ? __ldg(op + sidx) : 0u;
+        pen[i] = sidx < w.s1 ? __ldg(op + sidx + 1) : 0u;
+        pk[i] = sidx < w.s1 ? (CSER ? static_cast<int>(load_index(a.oi, a.oi_bits, sidx))
+                                    : static_cast<int>(sidx - w.s0 + 1))
+                            : 0;
+      }
+    }
     const float run = (w0 >= w.e0 && wn <= w.e1)
                           ? gather_prefix<ColT, XSMEM, false>(cur, w0, w.e0, w.e1, xs, x, pre, lane)
                           : gather_prefix<ColT, XSMEM, true>(cur, w0, w.e0, w.e1, xs, x, pre, lane);
@@ -424,12 +458,29 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
     }
     const float excl = __shfl_up_sync(0xffffffffu, incl, 1);
     off[lane] = lane ? excl : 0.f;
-    if (w.w0 == (w.e0 & ~(kAlign - 1)) && wn >= w.e1) {
+    CERDOT_TR(5, __float_as_uint(excl) & 0u);
+    if (single) {
       // ---- the whole row is in this window: its segments are independent (no carry, no ring)
       __syncwarp();
+      auto seg = [&](uint32_t st, uint32_t en, int k) {
+        if (en > st) {
+          const uint32_t lo = st - w0, b = en - 1u - w0;
+          const float pb = pre[ppos(b)];
+          float total;
+          if (lo == 0u) {
+            total = off[b >> 5] + pb;
+          } else {
+            const uint32_t a0 = lo - 1u;
+            const float pa = pre[ppos(a0)];
+            total = ((a0 >> 5) == (b >> 5)) ? pb - pa : (off[b >> 5] + pb) - (off[a0 >> 5] + pa);
+          }
+          acc = fmaf(wv[k], total, acc);
+        }
+      };
+#pragma unroll
+      for (int i = 0; i < kPre; ++i) seg(pst[i], pen[i], pk[i]);
       const PtrT *opp = op;
-#pragma unroll 4
-      for (uint32_t s = w.s0 + lane; s < w.s1; s += 32) {
+      for (uint32_t s = w.s0 + 32u * kPre + lane; s < w.s1; s += 32) {  // rows with > 128 segments
         const uint32_t st = __ldg(opp + s), en = __ldg(opp + s + 1);
         if (en > st) {
           const int k = CSER ? static_cast<int>(load_index(a.oi, a.oi_bits, s)) : static_cast<int>(s - w.s0 + 1);
@@ -482,6 +533,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
       if (ndone < 32) break;
     }
     __syncwarp();
+    CERDOT_TR(6, __float_as_uint(acc) & 0u);
     if (wn >= w.e1) {  // last window of the row
       float r = acc;
 #pragma unroll
@@ -510,6 +562,13 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
   }
   emit_empty(R1);
   cp_async_wait<0>();
+#ifdef CERDOT_TRACE_KERNELS
+  if (a.dbg && lane == 0 && (blockIdx.x % 37) == 0 && (wid == 0 || wid == kWarps - 1)) {
+    tr[4] = gtimer();
+    printf("TRACE cta %d warp %d rows %u start %llu prologue %llu wait %llu staged %llu end %llu gath %llu seg %llu\n",
+           blockIdx.x, wid, R1 - R0, tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[6]);
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1053,8 +1112,11 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
     const int want_nt = force ? atoi(force) : 0;
     if (want_nt == 1 && matvec_smem(a.k, a.n, true, 16, 3, oib) <= kHalfSmemBytes)
       return launch_matvec<ColT, PtrT, CSER, true, 512, 1, 2, 3>(a, x, y, st);
-    const bool wide = want_nt == 1024 || (want_nt == 0 && matvec_smem(a.k, a.n, true, 32, 4, oib) <= kMaxSmemBytes);
-    if (wide) return launch_matvec<ColT, PtrT, CSER, true, 1024, 1, 1, 4>(a, x, y, st);
+    // 28 warps per SM (896 threads, <= 72 regs) when x and the per-warp tables fit: enough warps that
+    // each holds at most one row of a 4096-row layer (a second row would run serially)
+    const bool wide = (want_nt == 896 || want_nt == 0) && matvec_smem(a.k, a.n, true, 28, 4, oib) <= kMaxSmemBytes &&
+                      a.m > int64_t(num_sms()) * 16;
+    if (wide) return launch_matvec<ColT, PtrT, CSER, true, 896, 1, 1, 4>(a, x, y, st);
     const bool xsmem = matvec_smem(a.k, a.n, true, 16, 4, oib) <= static_cast<size_t>(kMaxSmemBytes);
     return xsmem ? launch_matvec<ColT, PtrT, CSER, true, 512, 3, 1, 4>(a, x, y, st)
                  : launch_matvec<ColT, PtrT, CSER, false, 512, 3, 1, 4>(a, x, y, st);
@@ -1114,6 +1176,7 @@ int dot(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, fl
   a.bg = mat->background;
   a.segs = mat->segments;
   a.max_row_nnz = mat->max_row_nnz;
+  a.dbg = getenv("CERDOT_TRACE") ? 1 : 0;
   a.max_row_segs = mat->max_row_segments;
   if (a.m == 0 || batch == 0) return CERDOT_OK;
   if (a.bg != 0.0) {
