@@ -143,6 +143,14 @@ int cerdot_dot_cer(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t 
 int cerdot_dot_cser(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,
                     void *workspace, size_t workspace_bytes, void *stream);
 
+/* Host-buffer convenience (the e2e path of the reference-facing API): copies x (HOST, fp32, n x batch,
+ * row stride ldx; pinned for asynchronous copies) to the device, runs cerdot_dot, copies y (HOST,
+ * m x batch, row stride ldy) back and synchronises `stream`.  The device workspace (size from
+ * cerdot_dot_host_workspace_bytes) holds the device copies of x and y and the dot's own scratch. */
+size_t cerdot_dot_host_workspace_bytes(const cerdot_matrix *a, int64_t batch);
+int cerdot_dot_host(const cerdot_matrix *a, const float *x_host, int64_t ldx, int64_t batch, float *y_host,
+                    int64_t ldy, void *workspace, size_t workspace_bytes, void *stream);
+
 /* Row-shard planner (host).  row_ptr / omega_ptr are HOST arrays of the
  * given widths.  Writes parts+1 row bounds (bounds[0]=0, bounds[parts]=m)
  * splitting rows into contiguous blocks of near-equal encoded bytes

@@ -144,6 +144,46 @@ int cerdot_dot_cser(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t
   return cerdot_dot(a, x, ldx, batch, y, ldy, workspace, workspace_bytes, stream);
 }
 
+static size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+size_t cerdot_dot_host_workspace_bytes(const cerdot_matrix *a, int64_t batch) {
+  if (a == nullptr || batch <= 0) return 0;
+  const size_t b = static_cast<size_t>(batch);
+  return align256(static_cast<size_t>(a->n) * b * 4) + align256(static_cast<size_t>(a->m) * b * 4) +
+         align256(cerdot_dot_workspace_bytes(a, batch) + 1);
+}
+
+int cerdot_dot_host(const cerdot_matrix *a, const float *x_host, int64_t ldx, int64_t batch, float *y_host,
+                    int64_t ldy, void *workspace, size_t workspace_bytes, void *stream) {
+  int rc = check_matrix(a, batch, x_host, y_host, ldx, ldy);
+  if (rc) return rc;
+  if (a->m == 0 || batch == 0) return CERDOT_OK;
+  if (workspace == nullptr || workspace_bytes < cerdot_dot_host_workspace_bytes(a, batch))
+    return fail(CERDOT_E_WORKSPACE, "dot_host workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t b = static_cast<size_t>(batch);
+  char *base = static_cast<char *>(workspace);
+  float *dx = reinterpret_cast<float *>(base);
+  float *dy = reinterpret_cast<float *>(base + align256(static_cast<size_t>(a->n) * b * 4));
+  char *dws = reinterpret_cast<char *>(dy) + align256(static_cast<size_t>(a->m) * b * 4);
+  const size_t xrow = b * 4, yrow = b * 4;
+  if (batch == 1 || ldx == batch)
+    CERDOT_CUDA_CHECK(cudaMemcpyAsync(dx, x_host, static_cast<size_t>(a->n) * xrow, cudaMemcpyHostToDevice, st));
+  else
+    CERDOT_CUDA_CHECK(cudaMemcpy2DAsync(dx, xrow, x_host, static_cast<size_t>(ldx) * 4, xrow, a->n,
+                                        cudaMemcpyHostToDevice, st));
+  rc = cerdot::dot(a, dx, batch == 1 ? 1 : batch, batch, dy, batch == 1 ? 1 : batch, dws,
+                   cerdot_dot_workspace_bytes(a, batch), st);
+  if (rc) return rc;
+  if (batch == 1 || ldy == batch)
+    CERDOT_CUDA_CHECK(cudaMemcpyAsync(y_host, dy, static_cast<size_t>(a->m) * yrow, cudaMemcpyDeviceToHost, st));
+  else
+    CERDOT_CUDA_CHECK(cudaMemcpy2DAsync(y_host, static_cast<size_t>(ldy) * 4, dy, yrow, yrow, a->m,
+                                        cudaMemcpyDeviceToHost, st));
+  CERDOT_CUDA_CHECK(cudaStreamSynchronize(st));
+  return CERDOT_OK;
+}
+
 static uint64_t host_index(const void *p, int bits, int64_t i) {
   switch (bits) {
     case 8: return static_cast<const uint8_t *>(p)[i];

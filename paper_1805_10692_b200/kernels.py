@@ -84,7 +84,10 @@ class OpTrace:
 
 
 def _input_array(x):
-    """(float64 ndarray, input bits) for host inputs (kernels.py:98-103)."""
+    """(float ndarray, input bits) for host inputs (kernels.py:98-103); fp32/fp64 arrays pass through
+    unconverted (the device rounds to fp32 anyway)."""
+    if isinstance(x, np.ndarray) and x.dtype in (np.float32, np.float64):
+        return x, 32
     if isinstance(x, (Vector, DenseMatrix)) or (hasattr(x, "values") and hasattr(x, "element_bits")):
         return np.asarray(x.values, dtype=np.float64), int(x.element_bits)
     return np.asarray(x, dtype=np.float64), 32
@@ -191,22 +194,6 @@ class _Workspace:
 _WS = _Workspace()
 
 
-class _Pinned(threading.local):
-    """Per-thread pinned staging buffers for host inputs/outputs (no cudaHostAlloc per call)."""
-
-    def __init__(self):
-        self.bufs = {}
-
-    def get(self, key: str, nbytes: int):
-        torch = torch_mod()
-        buf = self.bufs.get(key)
-        if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 4096), dtype=torch.uint8, pin_memory=True)
-            self.bufs[key] = buf
-        return buf
-
-
-_PIN = _Pinned()
 
 
 def dot_device(enc, x, out=None, stream=None):
@@ -215,27 +202,75 @@ def dot_device(enc, x, out=None, stream=None):
     Stream-ordered on ``stream`` (default: torch's current stream), no host sync.
     """
     torch = torch_mod()
-    dev = enc.device_encoding(x.device)
+    dev = enc._dev if enc._dev is not None else enc.device_encoding(x.device)
     if x.dtype != torch.float32:
         x = x.to(torch.float32)
-    if x.ndim == 2 and x.stride(1) != 1:
-        x = x.contiguous()
-    if x.ndim == 1 and x.stride(0) != 1:
-        x = x.contiguous()
-    _check_shape(dev.n, tuple(x.shape))
-    batch = 1 if x.ndim == 1 else int(x.shape[1])
+    if x.ndim == 1:
+        if x.stride(0) != 1:
+            x = x.contiguous()
+        batch, ldx = 1, 1
+    else:
+        if x.stride(1) != 1:
+            x = x.contiguous()
+        batch, ldx = int(x.shape[1]), x.stride(0)
+    if x.shape[0] != dev.n or x.ndim > 2:
+        _check_shape(dev.n, tuple(x.shape))
     if out is None:
-        out = torch.empty((dev.m,) if x.ndim == 1 else (dev.m, batch), dtype=torch.float32, device=x.device)
-    ldx = 1 if x.ndim == 1 else x.stride(0)
+        out = torch.empty((dev.m,) if batch == 1 else (dev.m, batch), dtype=torch.float32, device=x.device)
     ldy = 1 if out.ndim == 1 else out.stride(0)
-    L = _native.lib()
     st = dev.struct()
-    ws_bytes = L.cerdot_dot_workspace_bytes(st, batch)
-    ws = _WS.get(x.device, ws_bytes) if ws_bytes else None
-    sp = stream if stream is not None else stream_ptr(x.device)
-    _native.check(L.cerdot_dot(st, x.data_ptr(), ldx, batch, out.data_ptr(), ldy,
-                               ws.data_ptr() if ws is not None else None, ws_bytes, sp))
+    ws_bytes = 8 * batch if dev.background != 0.0 else 0  # cerdot_dot_workspace_bytes
+    ws_ptr = _WS.get(x.device, ws_bytes).data_ptr() if ws_bytes else None
+    sp = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
+    _native.check(_native.lib().cerdot_dot(st, x.data_ptr(), ldx, batch, out.data_ptr(), ldy, ws_ptr, ws_bytes, sp))
     return out
+
+
+class _HostIO(threading.local):
+    """Per-thread cached buffers of the host-array path: pinned x / y and the device workspace per shape."""
+
+    def __init__(self):
+        self.dev = None
+        self.sets = {}
+
+    def get(self, m: int, n: int, batch: int, ws_bytes: int):
+        torch = torch_mod()
+        if self.dev is None or torch.cuda.current_device() != self.dev.index:
+            self.dev = require_cuda()
+            self.sets = {}
+        key = (m, n, batch)
+        bufs = self.sets.get(key)
+        if bufs is None or bufs[4].numel() < ws_bytes:
+            xs = (n,) if batch == 1 else (n, batch)
+            ys = (m,) if batch == 1 else (m, batch)
+            px = torch.empty(xs, dtype=torch.float32, pin_memory=True)
+            py = torch.empty(ys, dtype=torch.float32, pin_memory=True)
+            ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=self.dev)
+            bufs = (px, px.numpy(), py, py.numpy(), ws)
+            if len(self.sets) > 16:
+                self.sets.clear()
+            self.sets[key] = bufs
+        return bufs
+
+
+_IO = _HostIO()
+
+
+def _dot_host(a, xv: np.ndarray) -> np.ndarray:
+    """numpy x -> pinned staging -> one C call (H2D, kernel, D2H, sync: cerdot_dot_host) -> float64 numpy."""
+    torch = torch_mod()
+    batch = 1 if xv.ndim == 1 else int(xv.shape[1])
+    if _IO.dev is None:
+        _IO.dev = require_cuda()
+    dev = a._dev if a._dev is not None else a.device_encoding(_IO.dev)
+    st = dev.struct()
+    L = _native.lib()
+    ws_bytes = L.cerdot_dot_host_workspace_bytes(st, batch)
+    px, px_np, py, py_np, ws = _IO.get(a.m, a.n, batch, ws_bytes)
+    np.copyto(px_np, xv, casting="unsafe")  # the kernels compute in fp32
+    _native.check(L.cerdot_dot_host(st, px.data_ptr(), batch, batch, py.data_ptr(), batch, ws.data_ptr(),
+                                    ws.numel(), torch.cuda.current_stream(_IO.dev).cuda_stream))
+    return py_np.astype(np.float64)
 
 
 def _dot_encoded(a, x, trace, input_bits, output_bits, tracer):
@@ -250,17 +285,7 @@ def _dot_encoded(a, x, trace, input_bits, output_bits, tracer):
     else:
         xv, b_in = _input_array(x)
         _check_shape(a.n, xv.shape)
-        dev = require_cuda()
-        nx = xv.size * 4
-        xin = _PIN.get("x", nx)[:nx].view(torch.float32).view(xv.shape)
-        np.copyto(xin.numpy(), xv, casting="unsafe")  # the kernels compute in fp32
-        xt = xin.to(dev, non_blocking=True)
-        yt = dot_device(a, xt)
-        ny = yt.numel() * 4
-        yout = _PIN.get("y", ny)[:ny].view(torch.float32).view(tuple(yt.shape))
-        yout.copy_(yt, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
-        y = yout.numpy().astype(np.float64)
+        y = _dot_host(a, xv)
         cols = 1 if xv.ndim == 1 else xv.shape[1]
     if not trace:
         return y
