@@ -13,7 +13,7 @@ import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "_lib", "libcerdot.so")
+LIB_PATH = os.environ.get("CERDOT_LIB") or os.path.join(PKG, "_lib", "libcerdot.so")
 HEADER = os.path.join(ROOT, "include", "cerdot.h")
 
 OK, E_VALUE, E_TYPE, E_INDEX, E_CUDA, E_UNSUPPORTED, E_WORKSPACE = range(7)

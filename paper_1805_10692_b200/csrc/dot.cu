@@ -197,6 +197,32 @@ __device__ __forceinline__ float gather_prefix(const uint4 *raw_v, uint32_t w0, 
   return run;
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 constexpr int kFifoDepth = 4;
 
 __device__ __forceinline__ void cp_async4(void *smem_dst, const void *gmem_src) {
@@ -209,7 +235,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // Shared-memory carve-up of k_matvec (byte offsets; all 16 B aligned).
 struct MatvecSmem {
-  uint32_t wv, pre, off, ring_op, ring_oi, xs, total;
+  uint32_t bar, wv, pre, off, ring_op, ring_oi, xs, total;
 };
 __host__ __device__ __forceinline__ MatvecSmem matvec_layout(int64_t k, int64_t n_smem, uint32_t warps, uint32_t depth,
                                                              uint32_t oi_bytes) {
@@ -220,6 +246,7 @@ __host__ __device__ __forceinline__ MatvecSmem matvec_layout(int64_t k, int64_t 
     o += (bytes + 15u) & ~15u;
     return r;
   };
+  L.bar = take(8u);
   L.wv = take(static_cast<uint32_t>(min64(k, kSmemValues)) * 4u);
   L.pre = take(warps * kWin * 4u);
   L.off = take(warps * 32u * 4u);
@@ -254,6 +281,29 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kWarps + wid;
   const uint32_t R0 = static_cast<uint32_t>(gw * m / nw_total), R1 = static_cast<uint32_t>((gw + 1) * m / nw_total);
   pdl_launch_dependents();  // the next grid may start its own index prologue as our CTAs retire
+  // x staging: one TMA bulk copy (16 B-aligned part of x) issued at kernel start by thread 0 once the
+  // producer grid has finished, so it overlaps every warp's index chain below; the unaligned tail and
+  // the omega table are staged by all threads after their own chain.
+  uint64_t *xbar = reinterpret_cast<uint64_t *>(smem + L.bar);
+  const uint32_t x_tma_bytes =
+      XSMEM && (reinterpret_cast<uintptr_t>(x) & 15) == 0 ? static_cast<uint32_t>(a.n * 4) & ~15u : 0u;
+  if (XSMEM) {
+    if (threadIdx.x == 0) {
+      mbar_init(xbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      pdl_wait();
+      mbar_expect_tx(xbar, x_tma_bytes);
+      constexpr uint32_t kChunk = 32768;
+      for (uint32_t o = 0; o < x_tma_bytes; o += kChunk)
+        bulk_g2s(reinterpret_cast<unsigned char *>(xs) + o, reinterpret_cast<const unsigned char *>(x) + o,
+                 min(kChunk, x_tma_bytes - o), xbar);
+    }
+  }
+  const int kv = static_cast<int>(min64(a.k, kSmemValues));
+  const double wd0 = static_cast<int>(threadIdx.x) < kv ? __ldg(a.omega + threadIdx.x) : 0.0;
 #ifdef CERDOT_TRACE_KERNELS
   unsigned long long tr[7] = {gtimer(), 0, 0, 0, 0, 0, 0};
 #define CERDOT_TR(i, dep) \
@@ -395,18 +445,11 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
   // ------------------------------------------------------------ wait for the producer of x
   pdl_wait();
   CERDOT_TR(2, 0u);
-  const int kv = static_cast<int>(min64(a.k, kSmemValues));
-  for (int i = threadIdx.x; i < kv; i += blockDim.x) wv[i] = static_cast<float>(__ldg(a.omega + i) - a.bg);
+  if (static_cast<int>(threadIdx.x) < kv) wv[threadIdx.x] = static_cast<float>(wd0 - a.bg);
+  for (int i = threadIdx.x + blockDim.x; i < kv; i += blockDim.x) wv[i] = static_cast<float>(__ldg(a.omega + i) - a.bg);
   if (XSMEM) {
-    const int64_t n4 = a.n >> 2;
-    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
-      const float4 *x4 = reinterpret_cast<const float4 *>(x);
-      float4 *xs4 = reinterpret_cast<float4 *>(xs);
-      for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) xs4[i] = __ldg(x4 + i);
-      for (int64_t i = (n4 << 2) + threadIdx.x; i < a.n; i += blockDim.x) xs[i] = __ldg(x + i);
-    } else {
-      for (int64_t i = threadIdx.x; i < a.n; i += blockDim.x) xs[i] = __ldg(x + i);
-    }
+    for (int64_t i = (x_tma_bytes >> 2) + threadIdx.x; i < a.n; i += blockDim.x) xs[i] = __ldg(x + i);
+    mbar_wait(xbar, 0);
   }
   __syncthreads();
   CERDOT_TR(3, 0u);
@@ -586,32 +629,6 @@ constexpr uint32_t kTileCap = kTileNT * kTileEPT;            // aligned entry sl
 constexpr uint32_t kTileE = kTileCap - 32;                   // entries per tile (16 B alignment slack)
 constexpr uint32_t kTileS = 2048;                             // segments per tile
 constexpr uint32_t kTileRows = 1024;                          // rows staged per row group
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  uint32_t ok = 0;
-  while (!ok) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 
 struct TileSmem {
   uint32_t xs, wv, rp, ep, trow, stage, stage_bytes, col_off, op_off, oi_off, pre, tex, tinc, wex, winc, bar, total;
@@ -1118,8 +1135,10 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
                       a.m > int64_t(num_sms()) * 16;
     if (wide) return launch_matvec<ColT, PtrT, CSER, true, 896, 1, 1, 4>(a, x, y, st);
     const bool xsmem = matvec_smem(a.k, a.n, true, 16, 4, oib) <= static_cast<size_t>(kMaxSmemBytes);
-    return xsmem ? launch_matvec<ColT, PtrT, CSER, true, 512, 3, 1, 4>(a, x, y, st)
-                 : launch_matvec<ColT, PtrT, CSER, false, 512, 3, 1, 4>(a, x, y, st);
+    // u32 colI windows are 32 registers each: one window buffer (three would spill)
+    constexpr int kNbuf = sizeof(ColT) == 4 ? 1 : 3;
+    return xsmem ? launch_matvec<ColT, PtrT, CSER, true, 512, kNbuf, 1, 4>(a, x, y, st)
+                 : launch_matvec<ColT, PtrT, CSER, false, 512, kNbuf, 1, 4>(a, x, y, st);
   }
   const bool al4 = (ldx % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
   const bool al2 = (ldx % 2 == 0) && (reinterpret_cast<uintptr_t>(x) % 8 == 0);
