@@ -17,6 +17,8 @@
  *       replaces lemt.formats.index_bitwidth     (formats.py:52-59)
  *   cerdot_shard_plan
  *       new: contiguous row blocks balanced by encoded bytes
+ *   cerdot_row_entries
+ *       new: derived per-row entry offsets (shortens the mat-vec start-up chain)
  *
  * Conventions
  *   - Every pointer marked (device) is CUDA device memory on the current
@@ -79,6 +81,10 @@ typedef struct {
   double background;          /* host copy of omega[0] (CER) / omega[mode_index] (CSER) */
   int64_t max_row_nnz;        /* largest row (entries), 0 = unknown; selects the mat-vec tiling */
   int64_t max_row_segments;   /* largest row (segments), 0 = unknown */
+  const uint32_t *row_entry;  /* (device, optional) m+1 entry offsets, row_entry[r] = omega_ptr[row_ptr[r]]
+                                 (cerdot_row_entries); NULL = the kernels derive them.  A derived index,
+                                 not part of the format: it removes one dependent DRAM load from the
+                                 mat-vec's start-up chain */
 } cerdot_matrix;
 
 /* Result of phase 1 of the conversion. */
@@ -150,6 +156,10 @@ int cerdot_dot_cser(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t
 size_t cerdot_dot_host_workspace_bytes(const cerdot_matrix *a, int64_t batch);
 int cerdot_dot_host(const cerdot_matrix *a, const float *x_host, int64_t ldx, int64_t batch, float *y_host,
                     int64_t ldy, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Derived index for cerdot_matrix.row_entry: out[r] = omega_ptr[row_ptr[r]] for r in [0, m], u32
+ * (device, m+1).  CERDOT_E_VALUE when nnz does not fit 32 bits.  Stream-ordered. */
+int cerdot_row_entries(const cerdot_matrix *a, uint32_t *out, void *stream);
 
 /* Row-shard planner (host).  row_ptr / omega_ptr are HOST arrays of the
  * given widths.  Writes parts+1 row bounds (bounds[0]=0, bounds[parts]=m)

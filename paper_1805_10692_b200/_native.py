@@ -43,6 +43,7 @@ class CerdotMatrix(ctypes.Structure):
         ("background", ctypes.c_double),
         ("max_row_nnz", ctypes.c_int64),
         ("max_row_segments", ctypes.c_int64),
+        ("row_entry", ctypes.c_void_p),
     ]
 
 
@@ -83,6 +84,7 @@ _SIGNATURES = {
     "cerdot_dot_cser": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _SZ, _P]),
     "cerdot_dot_host_workspace_bytes": (_SZ, [ctypes.POINTER(CerdotMatrix), _I64]),
     "cerdot_dot_host": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _SZ, _P]),
+    "cerdot_row_entries": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _P]),
     "cerdot_shard_plan": (ctypes.c_int, [_P, _I32, _P, _I32, _I32, _I64, _I32, ctypes.POINTER(ctypes.c_int64)]),
 }
 

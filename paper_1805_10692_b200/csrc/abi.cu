@@ -192,6 +192,15 @@ static uint64_t host_index(const void *p, int bits, int64_t i) {
   }
 }
 
+int cerdot_row_entries(const cerdot_matrix *a, uint32_t *out, void *stream) {
+  int rc = check_matrix(a, 0, nullptr, nullptr, 0, 0);
+  if (rc) return rc;
+  if (a->nnz > static_cast<int64_t>(UINT32_MAX)) return fail(CERDOT_E_VALUE, "row_entry needs nnz < 2^32");
+  if (out == nullptr) return fail(CERDOT_E_VALUE, "null row_entry output");
+  if (a->m < 0) return fail(CERDOT_E_VALUE, "m must be >= 0");
+  return cerdot::row_entries(a, out, static_cast<cudaStream_t>(stream));
+}
+
 int cerdot_shard_plan(const void *row_ptr, int32_t row_ptr_bits, const void *omega_ptr, int32_t omega_ptr_bits,
                       int32_t col_bits, int64_t m, int32_t parts, int64_t *bounds) {
   if (parts < 1) return fail(CERDOT_E_VALUE, "parts must be >= 1");

@@ -65,6 +65,7 @@ struct DotArgs {
   const double *colsum;  // batch doubles when bg != 0
   int64_t segs;          // segment count (omegaPtr has segs + 1 entries)
   int64_t max_row_nnz, max_row_segs;
+  const uint32_t *re;  // optional row_entry index (m+1): re[r] = op[rp[r]]
   int dbg;  // CERDOT_TRACE: print per-CTA phase timestamps (debug only)
 };
 
@@ -321,14 +322,14 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
     g_ep = 0;
     if (idx <= R1 && R0 < R1) {
       g_rp = load_index(a.rp, a.rp_bits, idx);
-      g_ep = ld_idx(op, g_rp);
+      g_ep = a.re ? __ldg(a.re + idx) : ld_idx(op, g_rp);  // row_entry: no rowPtr -> omegaPtr dependence
     }
   };
   load_group(R0);
   const uint32_t s_beg = __shfl_sync(0xffffffffu, g_rp, 0);
   const uint32_t s_end = R0 < R1 ? load_index(a.rp, a.rp_bits, R1) : s_beg;
   const uint32_t e_beg = __shfl_sync(0xffffffffu, g_ep, 0);
-  const uint32_t e_end = R0 < R1 ? ld_idx(op, s_end) : e_beg;
+  const uint32_t e_end = R0 < R1 ? (a.re ? __ldg(a.re + R1) : ld_idx(op, s_end)) : e_beg;
 
   // ------------------------------------------------------------ L2 stream prefetch (TMA engine)
   constexpr uint32_t kChunkE = 4096 / sizeof(ColT), kAheadE = 24576 / sizeof(ColT);
@@ -728,10 +729,15 @@ __global__ void __launch_bounds__(kTileNT, 1) k_matvec_tile(DotArgs a, const flo
   for (uint32_t g0 = R0; g0 < R1; g0 += kTileRows) {
     const uint32_t g1 = min(R1, g0 + kTileRows), ng = g1 - g0;
     __syncthreads();  // previous group's tiles fully consumed
-    for (uint32_t i = tid; i <= ng; i += kTileNT) rp_s[i] = load_index(a.rp, a.rp_bits, g0 + i);
+    for (uint32_t i = tid; i <= ng; i += kTileNT) {
+      rp_s[i] = load_index(a.rp, a.rp_bits, g0 + i);
+      if (a.re) ep_s[i] = __ldg(a.re + g0 + i);  // row_entry: both loads in flight together
+    }
     __syncthreads();
-    for (uint32_t i = tid; i <= ng; i += kTileNT) ep_s[i] = ld_idx(op, rp_s[i]);
-    __syncthreads();
+    if (!a.re) {
+      for (uint32_t i = tid; i <= ng; i += kTileNT) ep_s[i] = ld_idx(op, rp_s[i]);
+      __syncthreads();
+    }
     if (tid == 0) {  // greedy tiles of whole rows
       uint32_t nt = 0, r = 0;
       trow[0] = 0;
@@ -1176,7 +1182,34 @@ int by_col(const DotArgs &a, int col_bits, int op_bits, const float *x, int64_t 
   }
 }
 
+template <typename PtrT>
+__global__ void __launch_bounds__(256) k_row_entries(const void *rp, int rp_bits, const PtrT *__restrict__ op,
+                                                     int64_t m, uint32_t *__restrict__ out) {
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r <= m;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[r] = static_cast<uint32_t>(op[load_index(rp, rp_bits, r)]);
+}
+
 }  // namespace
+
+int row_entries(const cerdot_matrix *mat, uint32_t *out, cudaStream_t st) {
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(mat->m + 1, 256), num_sms() * 8)));
+  switch (mat->omega_ptr_bits) {
+    case 8:
+      k_row_entries<<<grid, 256, 0, st>>>(mat->row_ptr, mat->row_ptr_bits, static_cast<const uint8_t *>(mat->omega_ptr),
+                                          mat->m, out);
+      break;
+    case 16:
+      k_row_entries<<<grid, 256, 0, st>>>(mat->row_ptr, mat->row_ptr_bits,
+                                          static_cast<const uint16_t *>(mat->omega_ptr), mat->m, out);
+      break;
+    default:
+      k_row_entries<<<grid, 256, 0, st>>>(mat->row_ptr, mat->row_ptr_bits,
+                                          static_cast<const uint32_t *>(mat->omega_ptr), mat->m, out);
+  }
+  CERDOT_LAUNCH_CHECK();
+  return CERDOT_OK;
+}
 
 int dot(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy, void *workspace,
         size_t workspace_bytes, cudaStream_t st) {
@@ -1197,6 +1230,7 @@ int dot(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, fl
   a.max_row_nnz = mat->max_row_nnz;
   a.dbg = getenv("CERDOT_TRACE") ? 1 : 0;
   a.max_row_segs = mat->max_row_segments;
+  a.re = mat->row_entry;
   if (a.m == 0 || batch == 0) return CERDOT_OK;
   if (a.bg != 0.0) {
     if (workspace == nullptr || workspace_bytes < sizeof(double) * static_cast<size_t>(batch))

@@ -21,6 +21,7 @@ int encode_sort_fill(const cerdot_encode_info *info, int kind, void *workspace, 
                      void *col, int col_bits, void *op, int op_bits, void *rp, int rp_bits, void *oi, int oi_bits,
                      cudaStream_t st);
 
+int row_entries(const cerdot_matrix *a, uint32_t *out, cudaStream_t st);
 int dot(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy, void *workspace,
         size_t workspace_bytes, cudaStream_t st);
 

@@ -8,6 +8,8 @@ H2D/D2H copy when it crosses the bus) holding, each 256-byte aligned,
     omegaPtr     S+1 uint{8,16,32}
     rowPtr       m+1 uint{8,16,32}
     omegaI       S   uint{8,16,32}   (CSER only)
+    rowEntry     m+1 uint32          (derived index: omegaPtr[rowPtr[r]], see
+                                      cerdot_row_entries; not part of the format)
 
 at exactly the reference's per-array widths, so the bytes the dot kernels
 stream are the reference's ``storage_bits`` (plus omega at 8 B instead of
@@ -16,6 +18,7 @@ the 4 B ``element_bits`` accounting).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -74,6 +77,17 @@ class DeviceEncoding:
     max_row_nnz: int = 0  # largest row in entries (0 = unknown)
     max_row_segments: int = 0  # largest row in segments (0 = unknown)
     _struct: object = field(default=None, repr=False)
+    _row_entry_ready: bool = False
+
+    def fill_row_entries(self, stream: int) -> None:
+        """Compute the derived rowEntry index on the device (stream-ordered)."""
+        if "rowEntry" not in self.offsets:
+            return
+        self._row_entry_ready = False
+        self._struct = None
+        _native.check(_native.lib().cerdot_row_entries(self.struct(), self.ptr("rowEntry"), stream))
+        self._row_entry_ready = True
+        self._struct = None
 
     @staticmethod
     def layout(kind: int, m: int, k: int, nnz: int, segments: int, bits: dict):
@@ -81,6 +95,8 @@ class DeviceEncoding:
                  ("rowPtr", m + 1, bits["rowPtr"])]
         if kind == _native.CSER:
             names.append(("omegaI", segments, bits["omegaI"]))
+        if nnz < 2**32:
+            names.append(("rowEntry", m + 1, 32))
         offsets, off = {}, 0
         for name, count, b in names:
             offsets[name] = off
@@ -89,19 +105,19 @@ class DeviceEncoding:
 
     def count(self, name: str) -> int:
         return {"omega": self.k, "colI": self.nnz, "omegaPtr": self.segments + 1, "rowPtr": self.m + 1,
-                "omegaI": self.segments}[name]
+                "omegaI": self.segments, "rowEntry": self.m + 1}[name]
 
     def ptr(self, name: str) -> int:
         return self.arena.data_ptr() + self.offsets[name]
 
     def nbytes(self, name: str) -> int:
-        b = 64 if name == "omega" else self.bits[name]
+        b = 64 if name == "omega" else (32 if name == "rowEntry" else self.bits[name])
         return self.count(name) * (b // 8)
 
     def to_host(self, name: str) -> np.ndarray:
         start = self.offsets[name]
         raw = self.arena[start:start + self.nbytes(name)].cpu().numpy()
-        dt = np.float64 if name == "omega" else _NP_UINT[self.bits[name]]
+        dt = np.float64 if name == "omega" else (np.uint32 if name == "rowEntry" else _NP_UINT[self.bits[name]])
         arr = raw.view(dt).copy()
         arr.setflags(write=False)
         return arr
@@ -124,6 +140,8 @@ class DeviceEncoding:
             s.background = self.background
             s.max_row_nnz = self.max_row_nnz
             s.max_row_segments = self.max_row_segments
+            use_re = self._row_entry_ready and not os.environ.get("CERDOT_NO_ROW_ENTRY")
+            s.row_entry = self.ptr("rowEntry") if use_re else None
             self._struct = s
         return self._struct
 
@@ -133,8 +151,8 @@ class DeviceEncoding:
 
     @property
     def format_bytes(self) -> int:
-        """Bytes the dot streams from HBM for the encoding (all arrays)."""
-        return sum(self.nbytes(nm) for nm in self.offsets)
+        """Bytes of the encoding's format arrays (the derived rowEntry index excluded)."""
+        return sum(self.nbytes(nm) for nm in self.offsets if nm != "rowEntry")
 
     @classmethod
     def from_host(cls, kind: int, m: int, n: int, mode_index: int, arrays: dict, device=None) -> "DeviceEncoding":
@@ -165,12 +183,15 @@ class DeviceEncoding:
         for name, a in host.items():
             buf[offsets[name]:offsets[name] + a.nbytes] = a.view(np.uint8)
         arena = staging.to(dev, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
         bg = float(omega[mode_index] if kind == _native.CSER else omega[0]) if k else 0.0
         rp = host["rowPtr"].astype(np.int64)
         optr = host["omegaPtr"].astype(np.int64)
         seg_rows = np.diff(rp) if m else np.zeros(0, dtype=np.int64)
         nnz_rows = (optr[rp[1:]] - optr[rp[:-1]]) if m else np.zeros(0, dtype=np.int64)
-        return cls(kind, m, n, k, nnz, segs, mode_index, bg, bits, arena, offsets,
-                   int(nnz_rows.max()) if nnz_rows.size else 0, int(seg_rows.max()) if seg_rows.size else 0)
+        enc = cls(kind, m, n, k, nnz, segs, mode_index, bg, bits, arena, offsets,
+                  int(nnz_rows.max()) if nnz_rows.size else 0, int(seg_rows.max()) if seg_rows.size else 0)
+        with torch.cuda.device(dev):
+            enc.fill_row_entries(stream_ptr(dev))
+            torch.cuda.current_stream(dev).synchronize()
+        return enc
 

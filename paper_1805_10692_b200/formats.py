@@ -274,8 +274,10 @@ def _encode(a, kind: int, index_bits, background):
                                            bits["colI"], dev.ptr("omegaPtr"), bits["omegaPtr"], dev.ptr("rowPtr"),
                                            bits["rowPtr"], dev.ptr("omegaI") if kind == _native.CSER else None,
                                            bits.get("omegaI", 8), st))
+        dev.fill_row_entries(st)
     # background as stored in omega (CER omega[0]; CSER omega[mode_index]) — same value
     dev.background = float(info.background)
+    dev._struct = None
     del ws  # stream-ordered release through the caching allocator
     if kind == _native.CSER:
         return CserMatrix(None, None, None, None, None, m, n, element_bits, dev.mode_index, _device=dev)

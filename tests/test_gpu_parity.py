@@ -279,3 +279,30 @@ def test_sort_path_large_alphabets(shape, distinct):
                 assert np.array_equal(enc.omega_index, ref["omegaI"]), tag
                 assert enc.mode_index == ref["mode_index"], tag
             assert rel_err(cd.dot(enc, x), numpy_port.dot(ref, x)) <= REL_TOL, tag
+
+
+@pytest.mark.parametrize("name", ["oracle", "alexnet-fc6"])
+def test_row_entry_index(name):
+    """The derived rowEntry index equals omegaPtr[rowPtr[r]], and the dot is bitwise the same with or without it."""
+    w, _ = synth.make_layer(name)
+    x = torch.from_numpy(np.random.default_rng(3).standard_normal(w.shape[1], dtype=np.float32)).cuda()
+    for encode in (cd.encode_cer, cd.encode_cser):
+        enc = encode(torch.from_numpy(w).cuda())
+        dev = enc.device_encoding()
+        re = dev.to_host("rowEntry")
+        assert np.array_equal(re, enc.omega_ptr.astype(np.int64)[enc.row_ptr.astype(np.int64)])
+        assert dev.struct().row_entry
+        for path in ("1", "2"):
+            import os
+            os.environ["CERDOT_MATVEC_PATH"] = path
+            try:
+                y_re = cd.dot_device(enc, x).cpu().numpy()
+                dev._row_entry_ready = False
+                dev._struct = None
+                assert not dev.struct().row_entry
+                y_plain = cd.dot_device(enc, x).cpu().numpy()
+                dev._row_entry_ready = True
+                dev._struct = None
+            finally:
+                del os.environ["CERDOT_MATVEC_PATH"]
+            assert np.array_equal(y_re, y_plain), (name, encode.__name__, path)
