@@ -478,13 +478,12 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
     // in flight during the gather below (they do not depend on x)
     const bool single = w.w0 == (w.e0 & ~(kAlign - 1)) && wn >= w.e1;
     constexpr int kPre = NBUF > 1 ? 1 : 4;  // register budget: the 3-buffer variant keeps one prefetch batch
-    uint32_t pst[kPre], pen[kPre];
+    uint32_t pen[kPre];
     int pk[kPre];
     if (single) {
 #pragma unroll
       for (int i = 0; i < kPre; ++i) {
         const uint32_t sidx = w.s0 + lane + 32u * i;
-        pst[i] = sidx < w.s1 ? __ldg(op + sidx) : 0u;
         pen[i] = sidx < w.s1 ? __ldg(op + sidx + 1) : 0u;
         pk[i] = sidx < w.s1 ? (CSER ? static_cast<int>(load_index(a.oi, a.oi_bits, sidx))
                                     : static_cast<int>(sidx - w.s0 + 1))
@@ -502,44 +501,38 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
     }
     const float excl = __shfl_up_sync(0xffffffffu, incl, 1);
     off[lane] = lane ? excl : 0.f;
+    __syncwarp();
     CERDOT_TR(5, __float_as_uint(excl) & 0u);
+    // window-global inclusive prefix at window position p: lane offset (conflict-free 32-entry table)
+    // plus the lane-local prefix
+    auto G = [&](uint32_t p) { return off[p >> 5] + pre[ppos(p)]; };
     if (single) {
-      // ---- the whole row is in this window: its segments are independent (no carry, no ring)
-      __syncwarp();
-      auto seg = [&](uint32_t st, uint32_t en, int k) {
-        if (en > st) {
-          const uint32_t lo = st - w0, b = en - 1u - w0;
-          const float pb = pre[ppos(b)];
-          float total;
-          if (lo == 0u) {
-            total = off[b >> 5] + pb;
-          } else {
-            const uint32_t a0 = lo - 1u;
-            const float pa = pre[ppos(a0)];
-            total = ((a0 >> 5) == (b >> 5)) ? pb - pa : (off[b >> 5] + pb) - (off[a0 >> 5] + pa);
-          }
-          acc = fmaf(wv[k], total, acc);
+      // ---- the whole row is in this window: lane i of a batch takes segment s0 + 32t + i, reads the
+      // window prefix at its end and gets its start value (the previous segment's end) by shuffle
+      float g_prev = 0.f;      // G before the row (the masked gather zeroed entries before e0)
+      uint32_t e_prev = w.e0;  // end of the previous segment
+      auto seg = [&](uint32_t en, int k, bool valid) {
+        const float ge = (valid && en > w0) ? G(en - 1u - w0) : 0.f;
+        float gs = __shfl_up_sync(0xffffffffu, ge, 1);
+        uint32_t st = __shfl_up_sync(0xffffffffu, en, 1);
+        if (lane == 0) {
+          gs = g_prev;
+          st = e_prev;
         }
+        g_prev = __shfl_sync(0xffffffffu, ge, 31);
+        e_prev = __shfl_sync(0xffffffffu, en, 31);
+        if (valid && en > st) acc = fmaf(wv[k], ge - gs, acc);
       };
 #pragma unroll
-      for (int i = 0; i < kPre; ++i) seg(pst[i], pen[i], pk[i]);
-      const PtrT *opp = op;
-      for (uint32_t s = w.s0 + 32u * kPre + lane; s < w.s1; s += 32) {  // rows with > 128 segments
-        const uint32_t st = __ldg(opp + s), en = __ldg(opp + s + 1);
-        if (en > st) {
-          const int k = CSER ? static_cast<int>(load_index(a.oi, a.oi_bits, s)) : static_cast<int>(s - w.s0 + 1);
-          const uint32_t lo = st - w0, b = en - 1u - w0;
-          const float pb = pre[ppos(b)];
-          float total;
-          if (lo == 0u) {
-            total = off[b >> 5] + pb;
-          } else {
-            const uint32_t a0 = lo - 1u;
-            const float pa = pre[ppos(a0)];
-            total = ((a0 >> 5) == (b >> 5)) ? pb - pa : (off[b >> 5] + pb) - (off[a0 >> 5] + pa);
-          }
-          acc = fmaf(wv[k], total, acc);
-        }
+      for (int i = 0; i < kPre; ++i) seg(pen[i], pk[i], w.s0 + lane + 32u * i < w.s1);
+      for (uint32_t base = w.s0 + 32u * kPre; base < w.s1; base += 32) {  // rows with > 32 kPre segments
+        const uint32_t sidx = base + lane;
+        const bool valid = sidx < w.s1;
+        const uint32_t en = valid ? static_cast<uint32_t>(__ldg(op + sidx + 1)) : 0u;
+        const int k = valid ? (CSER ? static_cast<int>(load_index(a.oi, a.oi_bits, sidx))
+                                    : static_cast<int>(sidx - w.s0 + 1))
+                            : 0;
+        seg(en, k, valid);
       }
       sc = w.s1;
     } else
