@@ -1133,6 +1133,10 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
     const bool wide = (want_nt == 896 || want_nt == 0) && matvec_smem(a.k, a.n, true, 28, 4, oib) <= kMaxSmemBytes &&
                       a.m > int64_t(num_sms()) * 16;
     if (wide) return launch_matvec<ColT, PtrT, CSER, true, 896, 1, 1, 4>(a, x, y, st);
+    // large x (VGG fc6: 100 KB): the same 28 warps with a 2-deep segment ring still fit
+    const bool wide2 = (want_nt == 896 || want_nt == 0) && matvec_smem(a.k, a.n, true, 28, 2, oib) <= kMaxSmemBytes &&
+                       a.m > int64_t(num_sms()) * 16;
+    if (wide2) return launch_matvec<ColT, PtrT, CSER, true, 896, 1, 1, 2>(a, x, y, st);
     const bool xsmem = matvec_smem(a.k, a.n, true, 16, 4, oib) <= static_cast<size_t>(kMaxSmemBytes);
     // u32 colI windows are 32 registers each: one window buffer (three would spill)
     constexpr int kNbuf = sizeof(ColT) == 4 ? 1 : 3;
