@@ -207,6 +207,9 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   uint32_t ok = 0;
   while (!ok) {
@@ -247,7 +250,7 @@ __host__ __device__ __forceinline__ MatvecSmem matvec_layout(int64_t k, int64_t 
     o += (bytes + 15u) & ~15u;
     return r;
   };
-  L.bar = take(8u);
+  L.bar = take(16u);
   L.wv = take(static_cast<uint32_t>(min64(k, kSmemValues)) * 4u);
   L.pre = take(warps * kWin * 4u);
   L.off = take(warps * 32u * 4u);
@@ -285,23 +288,23 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
   // x staging: one TMA bulk copy (16 B-aligned part of x) issued at kernel start by thread 0 once the
   // producer grid has finished, so it overlaps every warp's index chain below; the unaligned tail and
   // the omega table are staged by all threads after their own chain.
-  uint64_t *xbar = reinterpret_cast<uint64_t *>(smem + L.bar);
-  const uint32_t x_tma_bytes =
-      XSMEM && (reinterpret_cast<uintptr_t>(x) & 15) == 0 ? static_cast<uint32_t>(a.n * 4) & ~15u : 0u;
-  if (XSMEM) {
-    if (threadIdx.x == 0) {
-      mbar_init(xbar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      pdl_wait();
-      mbar_expect_tx(xbar, x_tma_bytes);
-      constexpr uint32_t kChunk = 32768;
-      for (uint32_t o = 0; o < x_tma_bytes; o += kChunk)
-        bulk_g2s(reinterpret_cast<unsigned char *>(xs) + o, reinterpret_cast<const unsigned char *>(x) + o,
-                 min(kChunk, x_tma_bytes - o), xbar);
-    }
+  uint64_t *xbar = reinterpret_cast<uint64_t *>(smem + L.bar), *wbar = xbar + 1;
+  const bool x_async = XSMEM && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const uint32_t x_tma_bytes = x_async ? static_cast<uint32_t>(a.n * 4) & ~15u : 0u;
+  if (threadIdx.x == 0) {
+    mbar_init(xbar, 1);           // x: thread 0's arrive + the TMA bytes
+    mbar_init(wbar, blockDim.x);  // omega table: every thread arrives once its share is stored
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (x_async && threadIdx.x == 0) {
+    pdl_wait();
+    for (int64_t i = x_tma_bytes >> 2; i < a.n; ++i) xs[i] = __ldg(x + i);  // <= 3 unaligned tail values
+    mbar_expect_tx(xbar, x_tma_bytes);
+    constexpr uint32_t kChunk = 32768;
+    for (uint32_t o = 0; o < x_tma_bytes; o += kChunk)
+      bulk_g2s(reinterpret_cast<unsigned char *>(xs) + o, reinterpret_cast<const unsigned char *>(x) + o,
+               min(kChunk, x_tma_bytes - o), xbar);
   }
   const int kv = static_cast<int>(min64(a.k, kSmemValues));
   const double wd0 = static_cast<int>(threadIdx.x) < kv ? __ldg(a.omega + threadIdx.x) : 0.0;
@@ -448,12 +451,12 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
   CERDOT_TR(2, 0u);
   if (static_cast<int>(threadIdx.x) < kv) wv[threadIdx.x] = static_cast<float>(wd0 - a.bg);
   for (int i = threadIdx.x + blockDim.x; i < kv; i += blockDim.x) wv[i] = static_cast<float>(__ldg(a.omega + i) - a.bg);
-  if (XSMEM) {
-    for (int64_t i = (x_tma_bytes >> 2) + threadIdx.x; i < a.n; i += blockDim.x) xs[i] = __ldg(x + i);
-    mbar_wait(xbar, 0);
+  mbar_arrive(wbar);  // no CTA-wide barrier: each warp waits for x / the omega table only when it needs them
+  if (XSMEM && !x_async) {  // misaligned x: cooperative staging
+    for (int64_t i = threadIdx.x; i < a.n; i += blockDim.x) xs[i] = __ldg(x + i);
+    __syncthreads();
   }
-  __syncthreads();
-  CERDOT_TR(3, 0u);
+  bool x_ready = !x_async, w_ready = false;
   const float y_empty = a.bg != 0.0 ? static_cast<float>(a.bg * a.colsum[0]) : 0.f;
 
   // ------------------------------------------------------------ consumer
@@ -490,6 +493,11 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
                             : 0;
       }
     }
+    if (!x_ready) {
+      mbar_wait(xbar, 0);
+      x_ready = true;
+      CERDOT_TR(3, 0u);
+    }
     const float run = (w0 >= w.e0 && wn <= w.e1)
                           ? gather_prefix<ColT, XSMEM, false>(cur, w0, w.e0, w.e1, xs, x, pre, lane)
                           : gather_prefix<ColT, XSMEM, true>(cur, w0, w.e0, w.e1, xs, x, pre, lane);
@@ -506,6 +514,10 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
     // window-global inclusive prefix at window position p: lane offset (conflict-free 32-entry table)
     // plus the lane-local prefix
     auto G = [&](uint32_t p) { return off[p >> 5] + pre[ppos(p)]; };
+    if (!w_ready) {
+      mbar_wait(wbar, 0);
+      w_ready = true;
+    }
     if (single) {
       // ---- the whole row is in this window: lane i of a batch takes segment s0 + 32t + i, reads the
       // window prefix at its end and gets its start value (the previous segment's end) by shuffle
@@ -599,6 +611,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
   }
   emit_empty(R1);
   cp_async_wait<0>();
+  if (x_async && threadIdx.x == 0) mbar_wait(xbar, 0);  // the CTA must not retire with the x copy in flight
 #ifdef CERDOT_TRACE_KERNELS
   if (a.dbg && lane == 0 && (blockIdx.x % 37) == 0 && (wid == 0 || wid == kWarps - 1)) {
     tr[4] = gtimer();
