@@ -482,15 +482,20 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
     const bool single = w.w0 == (w.e0 & ~(kAlign - 1)) && wn >= w.e1;
     constexpr int kPre = NBUF > 1 ? 1 : 4;  // register budget: the 3-buffer variant keeps one prefetch batch
     uint32_t pen[kPre];
-    int pk[kPre];
     if (single) {
 #pragma unroll
       for (int i = 0; i < kPre; ++i) {
         const uint32_t sidx = w.s0 + lane + 32u * i;
         pen[i] = sidx < w.s1 ? __ldg(op + sidx + 1) : 0u;
-        pk[i] = sidx < w.s1 ? (CSER ? static_cast<int>(load_index(a.oi, a.oi_bits, sidx))
-                                    : static_cast<int>(sidx - w.s0 + 1))
-                            : 0;
+      }
+      // CSER omegaI of the same segments: prefetched into L1 now (no registers held across the gather,
+      // where they would spill and stall on the load), read after it
+      if (CSER) {
+        const uint32_t ob = a.oi_bits / 8;
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(a.oi) + w.s0 * ob;
+        const uintptr_t hi = reinterpret_cast<uintptr_t>(a.oi) + min(w.s1, w.s0 + 32u * kPre) * ob;
+        const uintptr_t line = (lo & ~uintptr_t(127)) + static_cast<uintptr_t>(lane) * 128u;
+        if (line < hi) asm volatile("prefetch.global.L1 [%0];" ::"l"(line));
       }
     }
     if (!x_ready) {
@@ -536,7 +541,13 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
         if (valid && en > st) acc = fmaf(wv[k], ge - gs, acc);
       };
 #pragma unroll
-      for (int i = 0; i < kPre; ++i) seg(pen[i], pk[i], w.s0 + lane + 32u * i < w.s1);
+      for (int i = 0; i < kPre; ++i) {
+        const uint32_t sidx = w.s0 + lane + 32u * i;
+        const int k = sidx < w.s1 ? (CSER ? static_cast<int>(load_index(a.oi, a.oi_bits, sidx))
+                                          : static_cast<int>(sidx - w.s0 + 1))
+                                  : 0;
+        seg(pen[i], k, sidx < w.s1);
+      }
       for (uint32_t base = w.s0 + 32u * kPre; base < w.s1; base += 32) {  // rows with > 32 kPre segments
         const uint32_t sidx = base + lane;
         const bool valid = sidx < w.s1;

@@ -10,7 +10,7 @@ import paper_1805_10692_b200 as cd
 from paper_1805_10692_b200 import synth, shard
 cfg = synth.config(sys.argv[1]); rows = int(sys.argv[2])
 w, xs = synth.make_layer(cfg)
-enc = cd.encode_cer(torch.from_numpy(w).cuda())
+enc = (cd.encode_cser if sys.argv[3] == "cser" else cd.encode_cer)(torch.from_numpy(w).cuda())
 e = shard.slice_rows(enc, 0, rows) if rows < cfg.m else enc
 x = torch.from_numpy(xs[1]).cuda(); y = torch.empty(rows, device="cuda")
 for _ in range(3): cd.dot_device(e, x, out=y)
@@ -18,13 +18,14 @@ torch.cuda.synchronize()
 os.environ["CERDOT_TRACE"] = "1"
 cd.dot_device(e, x, out=y); torch.cuda.synchronize()
 '''
-for cfgname, rows, nore in (("alexnet-fc6", 4096, ""), ("alexnet-fc6", 4096, "1")):
-    env = dict(os.environ, CERDOT_MATVEC_PATH="1", CERDOT_NO_ROW_ENTRY=nore)
-    out = subprocess.run([sys.executable, "-c", code, cfgname, str(rows)], capture_output=True, text=True, env=env).stdout
+for cfgname, rows, kind in (("alexnet-fc6", 4096, "cer"), ("alexnet-fc6", 4096, "cser")):
+    env = dict(os.environ, CERDOT_MATVEC_PATH="1")
+    out = subprocess.run([sys.executable, "-c", code, cfgname, str(rows), kind], capture_output=True, text=True,
+                         env=env).stdout
     recs = [list(map(int, re.findall(r"(\d+)", l)[:10])) for l in out.splitlines() if l.startswith("TRACE")]
     if not recs:
         print(out); continue
     t0 = min(r[3] for r in recs)
-    print(f"== {cfgname} rows={rows} no_row_entry={nore!r}: us since first CTA start: start / prologue / after-wait / x-staged / end / gather+scan done / segments done")
+    print(f"== {cfgname} rows={rows} {kind}: us since first CTA start: start / prologue / after-wait / x-staged / end / gather+scan done / segments done")
     for r in recs:
         print(f"cta {r[0]:3d} warp {r[1]:2d} rows {r[2]}: " + " ".join(f"{(v - t0) / 1e3:7.2f}" for v in r[3:10]))
