@@ -232,10 +232,11 @@ class _HostIO(threading.local):
     def __init__(self):
         self.dev = None
         self.sets = {}
+        self.ws_bytes = {}
 
     def get(self, m: int, n: int, batch: int, ws_bytes: int):
         torch = torch_mod()
-        if self.dev is None or torch.cuda.current_device() != self.dev.index:
+        if self.dev is None or torch._C._cuda_getDevice() != self.dev.index:
             self.dev = require_cuda()
             self.sets = {}
         key = (m, n, batch)
@@ -257,7 +258,7 @@ _IO = _HostIO()
 
 
 def _dot_host(a, xv: np.ndarray) -> np.ndarray:
-    """numpy x -> pinned staging -> one C call (H2D, kernel, D2H, sync: cerdot_dot_host) -> float64 numpy."""
+    """numpy x -> pinned staging -> one C call (cerdot_dot_host: H2D, kernel, D2H, sync) -> float64 numpy."""
     torch = torch_mod()
     batch = 1 if xv.ndim == 1 else int(xv.shape[1])
     if _IO.dev is None:
@@ -265,11 +266,17 @@ def _dot_host(a, xv: np.ndarray) -> np.ndarray:
     dev = a._dev if a._dev is not None else a.device_encoding(_IO.dev)
     st = dev.struct()
     L = _native.lib()
-    ws_bytes = L.cerdot_dot_host_workspace_bytes(st, batch)
+    key = (a.m, a.n, batch, st.background != 0.0)  # what the workspace size depends on
+    ws_bytes = _IO.ws_bytes.get(key)
+    if ws_bytes is None:
+        ws_bytes = L.cerdot_dot_host_workspace_bytes(st, batch)
+        if len(_IO.ws_bytes) > 256:
+            _IO.ws_bytes.clear()
+        _IO.ws_bytes[key] = ws_bytes
     px, px_np, py, py_np, ws = _IO.get(a.m, a.n, batch, ws_bytes)
     np.copyto(px_np, xv, casting="unsafe")  # the kernels compute in fp32
     _native.check(L.cerdot_dot_host(st, px.data_ptr(), batch, batch, py.data_ptr(), batch, ws.data_ptr(),
-                                    ws.numel(), torch.cuda.current_stream(_IO.dev).cuda_stream))
+                                    ws.numel(), torch._C._cuda_getCurrentRawStream(_IO.dev.index)))
     return py_np.astype(np.float64)
 
 
