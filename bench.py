@@ -441,6 +441,7 @@ def run_ours(args):
                 steps_c = max(20, min(2000, int(args.case_budget_s / max(1e-6, _guess_t(name, b)))))
                 cases.append(measure_case(cd, torch, name, b, steps_c, 3, args.seed, device))
         fmt_b = {"cer": cd.storage_bits(cer) // 8, "cser": cd.storage_bits(cser) // 8}
+        traffic = _ncu_traffic(cfg.name)
         result = {
             "metric": "cer_cser_dot_achieved_gbs",
             "value": round(value, 2),
@@ -469,7 +470,8 @@ def run_ours(args):
             "roofline": {
                 "bound": "hbm", "kernel": "k_dot_vec (CER + CSER mat-vec)",
                 "achieved": round(step_bytes / t_step / 1e9, 2), "peak": peak, "unit": "GB/s",
-                "frac": round(step_bytes / t_step / 1e9 / peak, 4), "traffic": None,
+                "frac": round(step_bytes / t_step / 1e9 / peak, 4), "traffic": traffic.get("mean"),
+                "traffic_per_launch": traffic.get("per_launch"), "traffic_source": traffic.get("source"),
                 "peak_source": peak_src,
                 "per_launch_bytes": {"cer": alg_bytes(cer, 1), "cser": alg_bytes(cser, 1)},
             },
@@ -495,6 +497,19 @@ def run_ours(args):
 
         dist.destroy_process_group()
     return 0
+
+
+def _ncu_traffic(config_name: str) -> dict:
+    """DRAM bytes per launch of the headline kernels from the committed ncu --set full capture
+    (profiles/ncu_traffic.json); empty when there is none for this workload."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        per = d[config_name]
+        return {"mean": int(sum(per.values()) / len(per)), "per_launch": per, "source": d.get("_source")}
+    except (OSError, KeyError, ValueError):
+        return {}
 
 
 def _guess_t(name: str, batch: int) -> float:
