@@ -1,0 +1,30 @@
+"""One mat-mat call (for ncu): python tools/mm_one.py config batch kind [calls]; the kernel variant comes from
+CERDOT_MM_PATH.  The first call warms up; profile with --launch-skip accordingly."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1805_10692_b200 as cd  # noqa: E402
+from paper_1805_10692_b200 import synth  # noqa: E402
+
+
+def main():
+    name, batch, kind = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+    calls = int(sys.argv[4]) if len(sys.argv) > 4 else 2
+    cfg = synth.config(name)
+    rng = np.random.default_rng(0)
+    w = torch.from_numpy(synth.make_weights(cfg, rng)).cuda()
+    x = torch.from_numpy(synth.make_inputs(cfg, rng, batch)).cuda()
+    enc = (cd.encode_cer if kind == "cer" else cd.encode_cser)(w)
+    y = torch.empty((cfg.m, batch), device="cuda")
+    for _ in range(calls):
+        cd.dot_device(enc, x, out=y)
+    torch.cuda.synchronize()
+    print("ok", float(y.abs().sum()))
+
+
+if __name__ == "__main__":
+    main()
