@@ -294,9 +294,11 @@ def measure_case(cd, torch, cfg_name: str, batch: int, steps: int, warmup: int, 
 
     cfg = synth.config(cfg_name)
     rng = np.random.default_rng(seed)
-    w = synth.make_weights(cfg, rng)
+    if cfg.m * cfg.n > 10**9:  # config 5: the numpy draw takes a minute on the host; draw W on the device
+        wt = synth.make_weights_device(cfg, seed, device)
+    else:
+        wt = torch.from_numpy(synth.make_weights(cfg, rng)).to(device)
     x = synth.make_inputs(cfg, rng, batch)
-    wt = torch.from_numpy(w).to(device)
     out = {"config": cfg_name, "m": cfg.m, "n": cfg.n, "batch": batch}
     peak, _ = _peaks()
     for kind, encode in (("cer", cd.encode_cer), ("cser", cd.encode_cser)):
@@ -314,7 +316,7 @@ def measure_case(cd, torch, cfg_name: str, batch: int, steps: int, warmup: int, 
 
         secs = _graph_time(step, steps, warmup, rotate, torch)
         t = secs / steps
-        out[kind] = {"us": round(t * 1e6, 3), "alg_bytes": nbytes, "gbs": round(nbytes / t / 1e9, 2),
+        out[kind] = {"us": round(t * 1e6, 3), "steps": steps, "alg_bytes": nbytes, "gbs": round(nbytes / t / 1e9, 2),
                      "hbm_frac": round(nbytes / t / 1e9 / peak, 4), "gmacs": round(cfg.m * cfg.n * batch / t / 1e9, 2),
                      "adds_per_s_T": round(enc.nnz * batch / t / 1e12, 3), "rotating_copies": rotate}
         del copies, xs, ys
@@ -436,9 +438,11 @@ def run_ours(args):
         cases = []
         if args.cases == "all" and world == 1:
             plan = [("alexnet-fc6", 64), ("vgg-fc6", 1), ("vgg-fc6", 128), ("resnet-conv", 1),
-                    ("resnet-conv", 1568), ("oracle", 1)]
+                    ("resnet-conv", 1568), ("oracle", 1), ("large", 1), ("large", 256)]
             for name, b in plan:
                 steps_c = max(20, min(2000, int(args.case_budget_s / max(1e-6, _guess_t(name, b)))))
+                if name == "large":
+                    steps_c = 20 if b == 1 else 3
                 cases.append(measure_case(cd, torch, name, b, steps_c, 3, args.seed, device))
         fmt_b = {"cer": cd.storage_bits(cer) // 8, "cser": cd.storage_bits(cser) // 8}
         traffic = _ncu_traffic(cfg.name)

@@ -64,6 +64,7 @@ struct DotArgs {
   double bg;
   const double *colsum;  // batch doubles when bg != 0
   int64_t segs;          // segment count (omegaPtr has segs + 1 entries)
+  int64_t nnz;           // entries (len(colI))
   int64_t max_row_nnz, max_row_segs;
   const uint32_t *re;  // optional row_entry index (m+1): re[r] = op[rp[r]]
   int dbg;  // CERDOT_TRACE: print per-CTA phase timestamps (debug only)
@@ -911,6 +912,311 @@ int launch_matvec_tile(const DotArgs &a, const float *x, float *y, cudaStream_t 
   return CERDOT_OK;
 }
 
+// ---------------------------------------------------------------------------------------------------
+// Mat-vec for long rows (k_matvec_run): 32 warps per SM, 256-entry windows.
+//
+// The window kernel above holds a 1024-entry window per warp (32 colI registers per lane, a 4 KB prefix
+// table per warp), which caps it at 16 warps and 128 registers when x is large -- on the 32768^2 layer
+// (x = 128 KB) ncu shows it latency-bound: 0.31 issued warps per scheduler, 40% of the shared-memory
+// pipe.  This kernel keeps the same arithmetic (window-local fp32 prefix differences, one fma per
+// segment) with a quarter of the state, so a CTA runs 1024 threads at <= 64 registers:
+//   * lane l owns entries [wb + 8l, wb + 8l + 8) of the window: one 16 B colI load (u16), the next
+//     window's load in flight; 8 gathers from the x copy in shared memory; an in-lane running sum,
+//     lane offsets by a 5-step warp scan; the window prefix G stored to a 1 KB per-warp table;
+//   * segments are held lane-parallel, 32 at a time (lane j: segment sb + j, its start, end and value);
+//     all segments that close inside the window are finished in one pass: sum = G(end) - G(start - 1),
+//     or carry + G(end) for the segment open at the window start; the next 32 bounds are prefetched;
+//   * per-lane fp32 accumulators, one xor butterfly per row.
+// Rows are split evenly over all warps of the grid (one CTA per SM).
+constexpr int kRunNT = 1024;
+constexpr uint32_t kRunWin = 256;
+constexpr uint32_t kRunRingBytes = 2048;  // per warp: colI windows in flight (4 x 512 B for u16)
+
+template <typename ColT>
+struct RunRing {
+  static constexpr uint32_t kSlot = kRunWin * sizeof(ColT);     // bytes per window
+  static constexpr uint32_t kDepth = kRunRingBytes / kSlot;      // windows in flight (8 / 4 / 2)
+  static constexpr uint32_t kAlign = 16 / sizeof(ColT);           // window starts are 16 B aligned
+  static constexpr uint32_t kLane = 8 * sizeof(ColT);             // bytes per lane per window
+};
+
+// async copy of one lane's colI bytes into its ring slot; bytes past the warp's range are zero-filled
+template <uint32_t N>
+__device__ __forceinline__ void cp_async_lane(void *dst, const void *src, uint32_t valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  if (N == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid) : "memory");
+}
+
+struct RunSmem {
+  uint32_t bar, wv, pre, ring, xs, total;
+};
+__host__ __device__ __forceinline__ RunSmem run_layout(int64_t k, int64_t n, uint32_t warps, uint32_t depth) {
+  RunSmem L{};
+  uint32_t o = 0;
+  auto take = [&](uint32_t bytes) {
+    const uint32_t r = o;
+    o += (bytes + 15u) & ~15u;
+    return r;
+  };
+  (void)depth;
+  L.bar = take(16u);  // x barrier
+  L.wv = take(static_cast<uint32_t>(k) * 4u);
+  L.pre = take(warps * kRunWin * 4u);
+  L.ring = take(warps * kRunRingBytes);
+  L.xs = take(static_cast<uint32_t>(n) * 4u);
+  L.total = o;
+  return L;
+}
+
+// a lane's 8 column indices of the window held in the ring slot
+template <typename ColT>
+__device__ __forceinline__ void ring_cols8(const unsigned char *slot, int lane, uint32_t c[8]);
+template <>
+__device__ __forceinline__ void ring_cols8<uint8_t>(const unsigned char *slot, int lane, uint32_t c[8]) {
+  const uint2 v = *reinterpret_cast<const uint2 *>(slot + 8 * lane);
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    c[b] = (v.x >> (8 * b)) & 0xffu;
+    c[4 + b] = (v.y >> (8 * b)) & 0xffu;
+  }
+}
+template <>
+__device__ __forceinline__ void ring_cols8<uint16_t>(const unsigned char *slot, int lane, uint32_t c[8]) {
+  ColVec<uint16_t>::unpack(*reinterpret_cast<const uint4 *>(slot + 16 * lane), c);
+}
+template <>
+__device__ __forceinline__ void ring_cols8<uint32_t>(const unsigned char *slot, int lane, uint32_t c[8]) {
+  const uint4 v0 = *reinterpret_cast<const uint4 *>(slot + 32 * lane);
+  const uint4 v1 = *reinterpret_cast<const uint4 *>(slot + 32 * lane + 16);
+  c[0] = v0.x; c[1] = v0.y; c[2] = v0.z; c[3] = v0.w;
+  c[4] = v1.x; c[5] = v1.y; c[6] = v1.z; c[7] = v1.w;
+}
+
+template <typename ColT, typename PtrT, bool CSER>
+__global__ void __launch_bounds__(kRunNT, 1) k_matvec_run(DotArgs a, const float *__restrict__ x,
+                                                          float *__restrict__ y) {
+  using RR = RunRing<ColT>;
+  constexpr int kWarps = kRunNT / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const RunSmem L = run_layout(a.k, a.n, kWarps, RR::kDepth);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float *wv = reinterpret_cast<float *>(smem + L.wv);
+  float *pre = reinterpret_cast<float *>(smem + L.pre) + wid * kRunWin;
+  unsigned char *ring = smem + L.ring + wid * kRunRingBytes;
+  float *xs = reinterpret_cast<float *>(smem + L.xs);
+  uint64_t *xbar = reinterpret_cast<uint64_t *>(smem + L.bar);
+  const ColT *col = static_cast<const ColT *>(a.col);
+  const PtrT *op = static_cast<const PtrT *>(a.op);
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kWarps;
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kWarps + wid;
+  const uint32_t R0 = static_cast<uint32_t>(gw * a.m / nw), R1 = static_cast<uint32_t>((gw + 1) * a.m / nw);
+  pdl_launch_dependents();
+  const bool x_async = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const uint32_t x_tma = x_async ? static_cast<uint32_t>(a.n * 4) & ~15u : 0u;
+  if (threadIdx.x == 0) {
+    mbar_init(xbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // x: one TMA bulk copy once the producer grid is done; the unaligned tail by thread 0
+  if (threadIdx.x == 0) {
+    pdl_wait();
+    for (int64_t i = x_tma >> 2; i < a.n; ++i) xs[i] = __ldg(x + i);
+    mbar_expect_tx(xbar, x_tma);
+    constexpr uint32_t kChunk = 32768;
+    for (uint32_t o = 0; o < x_tma; o += kChunk)
+      bulk_g2s(reinterpret_cast<unsigned char *>(xs) + o, reinterpret_cast<const unsigned char *>(x) + o,
+               min(kChunk, x_tma - o), xbar);
+  }
+  for (int i = threadIdx.x; i < a.k; i += kRunNT) wv[i] = static_cast<float>(__ldg(a.omega + i) - a.bg);
+
+  // row entry bounds E(r), 32 rows per lane-parallel group (separate groups for producer and consumer)
+  auto row_e = [&](uint32_t r) -> uint32_t {
+    return a.re ? __ldg(a.re + r) : ld_idx(op, load_index(a.rp, a.rp_bits, r));
+  };
+  const uint32_t e_end = R0 < R1 ? row_e(R1) : 0u;  // end of this warp's colI range
+  uint32_t pg = R0, pgE = (R0 + lane <= R1 && R0 < R1) ? row_e(R0 + lane) : 0u;
+  uint32_t cg = pg, cgE = pgE;
+  auto group_e = [&](uint32_t r, uint32_t &g, uint32_t &gE) -> uint32_t {  // E(r), r in [R0, R1]
+    if (r - g >= 32u) {
+      g = r;
+      gE = (r + lane <= R1) ? row_e(r + lane) : 0u;
+    }
+    return __shfl_sync(0xffffffffu, gE, static_cast<int>(r - g));
+  };
+
+  // colI producer: windows of every non-empty row of the warp in order, kDepth in flight; each lane
+  // copies (cp.async) and later reads back only its own bytes, so no cross-lane synchronisation
+  uint32_t pr = R0, pwb = 0, pe1 = 0, pk = 0;
+  bool pdone = R0 >= R1;
+  auto prod_row = [&]() {  // position the producer at the first window of row pr (skipping empty rows)
+    while (pr < R1) {
+      const uint32_t e0 = group_e(pr, pg, pgE), e1 = group_e(pr + 1, pg, pgE);
+      if (e1 > e0) {
+        pwb = e0 & ~(RR::kAlign - 1u);
+        pe1 = e1;
+        return;
+      }
+      ++pr;
+    }
+    pdone = true;
+  };
+  const uint32_t e_lim = (e_end + RR::kAlign - 1u) & ~(RR::kAlign - 1u);  // readable (16 B rounded)
+  auto produce = [&]() {
+    if (!pdone) {
+      const uint32_t slot = pk % RR::kDepth, pos = pwb + 8u * lane;
+      const uint32_t valid = pos < e_lim ? RR::kLane : 0u;
+      unsigned char *dst = ring + slot * RR::kSlot + lane * RR::kLane;
+      const ColT *src = col + (pos < e_lim ? pos : pwb);
+      if (RR::kLane == 32) {
+        cp_async_lane<16>(dst, src, valid);
+        cp_async_lane<16>(dst + 16, src + 4, valid);
+      } else {
+        cp_async_lane<RR::kLane>(dst, src, valid);
+      }
+    }
+    cp_async_commit();  // one group per window (empty past the end) keeps wait_group counting exact
+    if (pdone) return;
+    ++pk;
+    pwb += kRunWin;
+    if (pwb >= pe1) {
+      ++pr;
+      prod_row();
+    }
+  };
+  if (!pdone) prod_row();
+  for (uint32_t d = 0; d < RR::kDepth; ++d) produce();
+  uint32_t ck = 0;  // windows consumed
+  __syncthreads();  // value table (x is waited on per warp below)
+  bool x_ready = false;
+
+  for (uint32_t r = R0; r < R1; ++r) {
+    const uint32_t e0 = group_e(r, cg, cgE), e1 = group_e(r + 1, cg, cgE);
+    float acc = 0.f;
+    if (e1 > e0) {
+      const uint32_t s0 = load_index(a.rp, a.rp_bits, r), s1 = load_index(a.rp, a.rp_bits, r + 1);
+      // segment batch: lane j holds segment sb + j (start st, end en, value v); invalid lanes never close
+      uint32_t sb = s0, st, en, nst, nen, nk;
+      auto fetch = [&](uint32_t b, uint32_t &fst, uint32_t &fen, uint32_t &fk) {
+        const uint32_t s = b + lane;
+        fst = s < s1 ? ld_idx(op, s) : 0xffffffffu;
+        fen = s < s1 ? ld_idx(op, s + 1) : 0xffffffffu;
+        fk = s < s1 ? (CSER ? load_index(a.oi, a.oi_bits, s) : s - s0 + 1) : 0u;
+      };
+      uint32_t k0;
+      fetch(sb, st, en, k0);
+      fetch(sb + 32, nst, nen, nk);
+      if (!x_ready) {
+        mbar_wait(xbar, 0);
+        x_ready = true;
+      }
+      float v = wv[k0];
+      uint32_t jdone = 0;
+      float carry = 0.f;
+      for (uint32_t wb = e0 & ~(RR::kAlign - 1u); wb < e1; wb += kRunWin) {
+        const uint32_t slot = ck % RR::kDepth;
+        cp_async_wait<RR::kDepth - 1>();
+        uint32_t c[8];
+        ring_cols8<ColT>(ring + slot * RR::kSlot, lane, c);
+        ++ck;
+        produce();
+        // gather + in-lane running sum (entries outside [e0, e1) count as 0)
+        const uint32_t p0 = wb + 8 * lane;
+        float g[8], run = 0.f;
+        if (p0 >= e0 && p0 + 8 <= e1) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            run += xs[c[i]];
+            g[i] = run;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t p = p0 + i;
+            if (p >= e0 && p < e1) run += xs[c[i]];
+            g[i] = run;
+          }
+        }
+        float incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const float t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const float off = incl - run;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) g[i] += off;
+        *reinterpret_cast<float4 *>(pre + lane * 8) = make_float4(g[0], g[1], g[2], g[3]);
+        *reinterpret_cast<float4 *>(pre + lane * 8 + 4) = make_float4(g[4], g[5], g[6], g[7]);
+        const float T = __shfl_sync(0xffffffffu, g[7], 31);  // window total, as stored at slot 255
+        __syncwarp();
+        // segments closing in this window (one pass per batch of 32)
+        const uint32_t wend = wb + kRunWin;
+        bool any = false;
+        float glast = 0.f;
+        while (true) {
+          const uint32_t closed = __ballot_sync(0xffffffffu, en <= wend);
+          const int cnt = __popc(closed);
+          const bool mine = lane >= static_cast<int>(jdone) && lane < cnt && en > st;
+          float ge = 0.f;
+          if (mine) {
+            ge = pre[en - 1 - wb];
+            const float gs = st > wb ? pre[st - 1 - wb] : -carry;
+            acc = fmaf(v, ge - gs, acc);
+          }
+          const uint32_t hit = __ballot_sync(0xffffffffu, mine);
+          const float gl = __shfl_sync(0xffffffffu, ge, 31 - __clz(hit | 1u));
+          if (hit) {
+            glast = gl;
+            any = true;
+          }
+          if (cnt == 32 && sb + 32 < s1) {  // batch exhausted inside this window: next 32 segments
+            sb += 32;
+            st = nst;
+            en = nen;
+            v = wv[nk];
+            fetch(sb + 32, nst, nen, nk);
+            jdone = 0;
+            continue;
+          }
+          jdone = static_cast<uint32_t>(cnt);
+          break;
+        }
+        carry = any ? T - glast : carry + T;
+        __syncwarp();  // the prefix table is rewritten by the next window
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[r] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + a.bg * a.colsum[0]) : acc;
+  }
+  if (!x_ready) mbar_wait(xbar, 0);  // no CTA exits with a bulk copy in flight
+  cp_async_wait<0>();
+}
+
+template <typename ColT, typename PtrT, bool CSER>
+int launch_matvec_run(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
+  const size_t smem = run_layout(a.k, a.n, kRunNT / 32, RunRing<ColT>::kDepth).total;
+  auto kern = k_matvec_run<ColT, PtrT, CSER>;
+  if (int rc_ = allow_max_smem(kern)) return rc_;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms(), ceil_div(a.m, kRunNT / 32))));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kRunNT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CERDOT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a, x, y));
+  return CERDOT_OK;
+}
+
 // Generic mat-vec for alphabets beyond the u16 slot table: warp per row, lanes over segments.
 template <typename ColT, typename PtrT, bool CSER>
 __global__ void __launch_bounds__(256) k_matvec_generic(DotArgs a, const float *__restrict__ x,
@@ -1152,8 +1458,13 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
     // measured on B200: the tile pipeline wins when there are fewer rows than warps in the window kernel
     // (ResNet conv 512 rows: 8.2 vs 13+ us); with >= 1 row per warp the window kernel wins (AlexNet, VGG)
     const bool few_rows = a.m < int64_t(num_sms()) * 16;
-    const int want = force_path ? atoi(force_path) : (few_rows ? 2 : 1);
+    // long rows (>= 4096 entries on average, the 32768^2 layer: 9829): the 32-warp run kernel
+    // (431 -> 314 us there); at ~1000-entry rows (AlexNet, VGG fc6) the window kernel is 0-30% faster
+    const bool long_rows = a.nnz >= int64_t(4096) * a.m;
+    const int want = force_path ? atoi(force_path) : (few_rows ? 2 : (long_rows ? 3 : 1));
     if (tile_ok && want == 2) return launch_matvec_tile<ColT, PtrT, CSER>(a, x, y, st);
+    if (want == 3 && run_layout(a.k, a.n, kRunNT / 32, RunRing<ColT>::kDepth).total <= static_cast<uint32_t>(kMaxSmemBytes))
+      return launch_matvec_run<ColT, PtrT, CSER>(a, x, y, st);
     // Prefer the co-resident variant (16 warps, <= 64 regs, <= half the SM's shared memory): two
     // consecutive calls' CTAs then share an SM and, with programmatic dependent launch, the next call's
     // index prologue (rowPtr -> omegaPtr -> colI latency chain) overlaps this call's work.
@@ -1261,6 +1572,7 @@ int dot(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, fl
   a.bg = mat->background;
   a.segs = mat->segments;
   a.max_row_nnz = mat->max_row_nnz;
+  a.nnz = mat->nnz;
   a.dbg = getenv("CERDOT_TRACE") ? 1 : 0;
   a.max_row_segs = mat->max_row_segments;
   a.re = mat->row_entry;

@@ -120,6 +120,35 @@ def make_weights(cfg: LayerConfig, rng: np.random.Generator, rows: int | None = 
     return out
 
 
+def make_weights_device(cfg: LayerConfig, seed: int, device, row0: int = 0, rows: int | None = None,
+                        chunk_rows: int = 1024):
+    """Rows [row0, row0 + rows) of a config's W drawn ON THE DEVICE (torch), for the 32768^2 config whose
+    numpy draw takes a minute on the host.  Same codebook and pmf as ``make_weights`` (inverse-CDF sampling
+    of a uniform), but a different random stream, so it is statistically, not draw-for-draw, the numpy
+    layer.  Each block of ``chunk_rows`` global rows has its own generator seeded ``(seed, block)``, so a
+    row block is the same whichever shard draws it (row-sharded runs at any GPU count see one matrix)."""
+    import torch
+
+    m = cfg.m - row0 if rows is None else int(rows)
+    lv = torch.from_numpy(levels_of(cfg)).to(device)
+    cdf = torch.from_numpy(np.cumsum(pmf_of(cfg))).to(device)
+    cdf[-1] = 1.0
+    out = torch.empty((m, cfg.n), dtype=torch.float32, device=device)
+    g = torch.Generator(device=device)
+    r = row0
+    while r < row0 + m:
+        blk = r // chunk_rows
+        b0, b1 = blk * chunk_rows, min(cfg.m, (blk + 1) * chunk_rows)
+        g.manual_seed(seed * 1_000_003 + blk)
+        u = torch.rand((b1 - b0, cfg.n), generator=g, device=device, dtype=torch.float64)
+        lo, hi = max(r, b0), min(row0 + m, b1)
+        idx = torch.searchsorted(cdf, u[lo - b0:hi - b0], right=True).clamp_(max=cfg.k - 1)
+        out[lo - row0:hi - row0] = lv[idx]
+        del u, idx
+        r = hi
+    return out
+
+
 def make_inputs(cfg: LayerConfig, rng: np.random.Generator, batch: int) -> np.ndarray:
     """One X draw (fp32, n x B, row-major); B=1 returns the (n,) vector of column 0."""
     x = rng.standard_normal((cfg.n, batch), dtype=np.float32)

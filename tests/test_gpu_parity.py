@@ -152,6 +152,42 @@ def test_full_batch_resnet_conv_properties():
     assert rel_err(y[:, 1500:].cpu().numpy(), ref) <= REL_TOL
 
 
+def test_long_rows_default_to_run_kernel_and_match_oracle():
+    """Rows of >= 4096 entries take the run kernel by default (colI ring across rows, segment batches
+    that close several times inside one window, CER padding); integer alphabet -> bitwise, real -> 1e-5."""
+    rng = np.random.default_rng(21)
+    m, n = 96, 20000
+    levels = np.arange(-12, 13, dtype=np.float64)
+    p = np.exp(-np.abs(levels) / 3.0)
+    p[12] = 4.0 * p.sum()  # zero is the mode (~70%)
+    w = rng.choice(levels, size=(m, n), p=p / p.sum())
+    w[17, :] = 0.0  # an empty row between long ones
+    x = rng.integers(-3, 4, size=n).astype(np.float64)
+    for encode in (cd.encode_cer, cd.encode_cser):
+        enc = encode(w)
+        assert enc.nnz >= 4096 * m * 0.5
+        assert np.array_equal(cd.dot(enc, x), w @ x), encode.__name__
+        xr = rng.standard_normal(n)
+        ref = c_oracle.dot(c_oracle.encode(w, "cer" if encode is cd.encode_cer else "cser"), xr)
+        assert rel_err(cd.dot(enc, xr.astype(np.float32)), ref) <= REL_TOL, encode.__name__
+
+
+def test_large_config_properties():
+    """Config 5 (32768^2, 256 levels) at full size: CER and CSER agree, scaling x by 2 is exact, and a
+    row slice matches the oracle (size-independent checks; W drawn on the device)."""
+    cfg = synth.config("large")
+    w = synth.make_weights_device(cfg, 0, "cuda")
+    x = torch.from_numpy(np.random.default_rng(5).standard_normal(cfg.n, dtype=np.float32)).cuda()
+    cer, cser = cd.encode_cer(w), cd.encode_cser(w)
+    y_cer, y_cser = cd.dot(cer, x), cd.dot(cser, x)
+    assert rel_err(y_cer.cpu().numpy(), y_cser.double().cpu().numpy()) <= REL_TOL
+    assert torch.equal(cd.dot(cer, 2.0 * x), 2.0 * y_cer)
+    rows = w[:64].cpu().numpy()
+    del w
+    ref = c_oracle.dot(c_oracle.encode(rows, "cser"), x.cpu().numpy().astype(np.float64))
+    assert rel_err(y_cser[:64].cpu().numpy(), ref) <= REL_TOL
+
+
 def test_background_nonzero_without_decomposition():
     # criterion-7 shaped matrices (mode != 0) encoded directly: y += bg * sum(x) in the epilogue
     for seed in range(10):
@@ -225,11 +261,11 @@ def test_wide_alphabets_up_to_fast_limit():
         assert np.array_equal(cd.dot(enc, x), w @ x)
 
 
-@pytest.mark.parametrize("path", ["tile", "window"])
+@pytest.mark.parametrize("path", ["tile", "window", "run"])
 @pytest.mark.parametrize("name", ["oracle", "alexnet-fc6", "resnet-conv"])
 def test_matvec_paths_agree_with_oracle(monkeypatch, config_goldens, name, path):
-    """Both mat-vec kernels (CTA-tile TMA pipeline and the warp-window kernel) meet the bar."""
-    monkeypatch.setenv("CERDOT_MATVEC_PATH", "1" if path == "window" else "2")
+    """Every mat-vec kernel (CTA-tile TMA pipeline, warp-window kernel, 32-warp run kernel) meets the bar."""
+    monkeypatch.setenv("CERDOT_MATVEC_PATH", {"window": "1", "tile": "2", "run": "3"}[path])
     meta, ys = config_goldens
     w, _ = synth.make_layer(name)
     x1 = np.random.default_rng(1).standard_normal(w.shape[1], dtype=np.float32)
@@ -239,9 +275,9 @@ def test_matvec_paths_agree_with_oracle(monkeypatch, config_goldens, name, path)
         assert rel_err(cd.dot(enc, x1), ys[f"{name}/{kind}/b1"]) <= REL_TOL, (name, kind, path)
 
 
-@pytest.mark.parametrize("path", ["1", "2"])
+@pytest.mark.parametrize("path", ["1", "2", "3"])
 def test_matvec_tile_edge_rows(monkeypatch, path):
-    """Empty rows, single-entry rows, a long row next to short ones, non-zero background (both kernels)."""
+    """Empty rows, single-entry rows, a long row next to short ones, non-zero background (every kernel)."""
     monkeypatch.setenv("CERDOT_MATVEC_PATH", path)
     rng = np.random.default_rng(9)
     w = np.zeros((300, 700))

@@ -1,4 +1,4 @@
-"""One mat-mat call (for ncu): python tools/mm_one.py config batch kind [calls]; the kernel variant comes from
+"""One dot call (mat-vec or mat-mat, for ncu): python tools/mm_one.py config batch kind [calls]; the kernel variant comes from
 CERDOT_MM_PATH.  The first call warms up; profile with --launch-skip accordingly."""
 import os
 import sys
@@ -16,10 +16,14 @@ def main():
     calls = int(sys.argv[4]) if len(sys.argv) > 4 else 2
     cfg = synth.config(name)
     rng = np.random.default_rng(0)
-    w = torch.from_numpy(synth.make_weights(cfg, rng)).cuda()
+    if cfg.m * cfg.n > 10**9:
+        w = synth.make_weights_device(cfg, 0, "cuda")
+    else:
+        w = torch.from_numpy(synth.make_weights(cfg, rng)).cuda()
     x = torch.from_numpy(synth.make_inputs(cfg, rng, batch)).cuda()
     enc = (cd.encode_cer if kind == "cer" else cd.encode_cser)(w)
-    y = torch.empty((cfg.m, batch), device="cuda")
+    del w
+    y = torch.empty((cfg.m, batch) if batch > 1 else (cfg.m,), device="cuda")
     for _ in range(calls):
         cd.dot_device(enc, x, out=y)
     torch.cuda.synchronize()

@@ -1,6 +1,8 @@
 """Graph-replayed cold mat-vec time (us per call) for each config x kind; prints one JSON line per case.
 
 Usage: python tools/mv_time.py [config ...]   (CERDOT_LIB selects the library for A/B runs)
+MV_VARIANTS="1 3" times each CERDOT_MATVEC_PATH value in one process ("auto" = unset) and reports each
+variant's max|y - y_first| / max|y_first| against the first.
 """
 import json
 import os
@@ -41,18 +43,33 @@ def main():
     for name in names:
         cfg = synth.config(name)
         rng = np.random.default_rng(0)
-        w = torch.from_numpy(synth.make_weights(cfg, rng)).cuda()
+        if cfg.m * cfg.n > 10**9:
+            w = synth.make_weights_device(cfg, 0, "cuda")
+        else:
+            w = torch.from_numpy(synth.make_weights(cfg, rng)).cuda()
         x = synth.make_inputs(cfg, rng, 1)
         for kind in ("cer", "cser"):
             enc = (cd.encode_cer if kind == "cer" else cd.encode_cser)(w)
             R = 16 if cfg.m * cfg.n < 10**8 else 2
             copies = [bench._clone(cd, enc) for _ in range(R)]
             xs = [torch.from_numpy(x).cuda().reshape(-1) for _ in range(R)]
-            ys = [torch.empty(cfg.m, device="cuda") for _ in range(R)]
-            us = graph_us(copies, xs, ys)
-            gb = cd.storage_bits(enc) / 8 + 4 * (cfg.n + cfg.m)
-            print(json.dumps({"lib": os.path.basename(tag), "config": name, "kind": kind, "us": round(us, 3),
-                              "gbs": round(gb / us / 1e3, 1)}), flush=True)
+            ref = None
+            for var in os.environ.get("MV_VARIANTS", "auto").split():
+                if var == "auto":
+                    os.environ.pop("CERDOT_MATVEC_PATH", None)
+                else:
+                    os.environ["CERDOT_MATVEC_PATH"] = var
+                ys = [torch.full((cfg.m,), float("nan"), device="cuda") for _ in range(R)]
+                us = graph_us(copies, xs, ys)
+                y = ys[0].double().cpu().numpy()
+                if ref is None:
+                    ref = y
+                err = float(np.abs(y - ref).max() / np.abs(ref).max())
+                gb = cd.storage_bits(enc) / 8 + 4 * (cfg.n + cfg.m)
+                print(json.dumps({"lib": os.path.basename(tag), "config": name, "kind": kind, "variant": var,
+                                  "us": round(us, 3), "gbs": round(gb / us / 1e3, 1), "rel_vs_first": err}),
+                      flush=True)
+            del copies, xs
 
 
 if __name__ == "__main__":
