@@ -1366,6 +1366,160 @@ __global__ void __launch_bounds__(256, (V == 4 ? 4 : 1)) k_matmat(DotArgs a, con
   }
 }
 
+// Mat-mat, flat entry stream (k_matmat_flat): warp per (row, 32*V batch columns), as k_matmat, but the
+// row's entries are walked 32 at a time without regard to segment boundaries: the 32 column indices of
+// a chunk sit one per lane, the segments ending inside the chunk are turned into a 32-bit mask
+// (redux.or over the lane-parallel segment bounds) and their values into a per-warp 32-slot table, so
+// each entry costs one shuffle, one V-wide X-row load, V adds and a bit test, with eight loads in flight.
+// ncu on k_matmat (AlexNet fc6, B = 64): 44 instructions per entry, issue-bound; this walk is ~10.
+// Per column the arithmetic is k_matmat's exactly (sequential fp32 segment sums in colI order, one
+// fma per non-empty segment): the two kernels agree bitwise.
+template <int V>
+__device__ __forceinline__ void ld_xrow(const float *p, bool full, int nval, float *out) {
+  if (full) {
+    if (V == 4) {
+      const float4 t = __ldg(reinterpret_cast<const float4 *>(p));
+      out[0] = t.x; out[1 % V] = t.y; out[2 % V] = t.z; out[3 % V] = t.w;
+    } else if (V == 2) {
+      const float2 t = __ldg(reinterpret_cast<const float2 *>(p));
+      out[0] = t.x; out[1 % V] = t.y;
+    } else {
+      out[0] = __ldg(p);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < V; ++q) out[q] = q < nval ? __ldg(p + q) : 0.f;
+  }
+}
+
+template <typename ColT, typename PtrT, bool CSER, int V, int D>
+__global__ void __launch_bounds__(256) k_matmat_flat(DotArgs a, const float *__restrict__ x,
+                                                                      int64_t ldx, int64_t batch,
+                                                                      float *__restrict__ y, int64_t ldy) {
+  __shared__ float vtab_all[8][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float *vtab = vtab_all[wid];
+  const ColT *col = static_cast<const ColT *>(a.col);
+  const PtrT *op = static_cast<const PtrT *>(a.op);
+  const int64_t chunks = ceil_div(batch, 32 * V);
+  const int64_t units = a.m * chunks;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t u = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < units; u += nwarps) {
+    const int64_t row = u / chunks, cb = (u - row * chunks) * 32 * V + lane * V;
+    const uint32_t s0 = load_index(a.rp, a.rp_bits, row), s1 = load_index(a.rp, a.rp_bits, row + 1);
+    float acc[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) acc[q] = 0.f;
+    if (s1 > s0) {
+      const float *xb = x + cb;
+      const bool full = cb + V <= batch;
+      const int nval = static_cast<int>(max64(0, min64(V, batch - cb)));
+      const uint32_t ldx32 = static_cast<uint32_t>(ldx);
+      const uint32_t e0 = a.re ? __ldg(a.re + row) : ld_idx(op, s0);
+      const uint32_t e1 = a.re ? __ldg(a.re + row + 1) : ld_idx(op, s1);
+      // segment batch (lane j: segment sb + j) with the next batch prefetched
+      auto fetch = [&](uint32_t b, uint32_t &fst, uint32_t &fen, float &fv) {
+        const uint32_t s = b + lane;
+        fst = s < s1 ? ld_idx(op, s) : 0xffffffffu;
+        fen = s < s1 ? ld_idx(op, s + 1) : 0xffffffffu;
+        fv = 0.f;
+        if (s < s1) {
+          const uint32_t k = CSER ? load_index(a.oi, a.oi_bits, s) : s - s0 + 1;
+          fv = static_cast<float>(__ldg(a.omega + k) - a.bg);
+        }
+      };
+      uint32_t sb = s0, st, en, nst, nen;
+      float v, nv;
+      fetch(sb, st, en, v);
+      fetch(sb + 32, nst, nen, nv);
+      float s[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) s[q] = 0.f;
+      uint32_t cur = (e0 + lane < e1) ? ld_idx(col, e0 + lane) : 0u;
+      for (uint32_t ch = e0; ch < e1; ch += 32) {
+        const uint32_t nxt = (ch + 32 + lane < e1) ? ld_idx(col, ch + 32 + lane) : 0u;
+        const uint32_t cend = min(ch + 32, e1);
+        // segments ending in [ch, cend): mask of their last entries, values into vtab
+        uint32_t mask = 0;
+        while (true) {
+          const bool ends_here = en > st && en - 1 >= ch && en - 1 < cend;
+          if (ends_here) vtab[en - 1 - ch] = v;
+          mask |= __reduce_or_sync(0xffffffffu, ends_here ? 1u << (en - 1 - ch) : 0u);
+          // batch exhausted before the chunk end: next 32 segments (their ends may fall in this chunk)
+          const bool need = __shfl_sync(0xffffffffu, en, 31) < cend && sb + 32 < s1;
+          if (!need) break;
+          sb += 32;
+          st = nst;
+          en = nen;
+          v = nv;
+          fetch(sb + 32, nst, nen, nv);
+        }
+        __syncwarp();
+        const uint32_t cnt = cend - ch;
+        // D X-row loads in flight: 8, or 4 for V = 4 when there are many units (78 instead of 112
+        // registers, 3 CTAs per SM instead of 2)
+        if (cnt == 32) {
+#pragma unroll
+          for (int i0 = 0; i0 < 32; i0 += D) {
+            float xv[D][V];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              const uint32_t c = __shfl_sync(0xffffffffu, cur, i0 + i);
+              ld_xrow<V>(xb + static_cast<size_t>(c) * ldx32, full, nval, xv[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+#pragma unroll
+              for (int q = 0; q < V; ++q) s[q] += xv[i][q];
+              if ((mask >> (i0 + i)) & 1u) {
+                const float vv = vtab[i0 + i];
+#pragma unroll
+                for (int q = 0; q < V; ++q) {
+                  acc[q] = fmaf(vv, s[q], acc[q]);
+                  s[q] = 0.f;
+                }
+              }
+            }
+          }
+        } else {  // the row's last, partial chunk
+          for (uint32_t i0 = 0; i0 < cnt; i0 += D) {
+            float xv[D][V];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              const uint32_t c = __shfl_sync(0xffffffffu, cur, (i0 + i) & 31u);
+              if (i0 + i < cnt) ld_xrow<V>(xb + static_cast<size_t>(c) * ldx32, full, nval, xv[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              if (i0 + i < cnt) {
+#pragma unroll
+                for (int q = 0; q < V; ++q) s[q] += xv[i][q];
+                if ((mask >> (i0 + i)) & 1u) {
+                  const float vv = vtab[i0 + i];
+#pragma unroll
+                  for (int q = 0; q < V; ++q) {
+                    acc[q] = fmaf(vv, s[q], acc[q]);
+                    s[q] = 0.f;
+                  }
+                }
+              }
+            }
+          }
+        }
+        __syncwarp();  // vtab is rewritten for the next chunk
+        cur = nxt;
+      }
+    }
+    float *yr = y + row * ldy;
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      const int64_t c = cb + q;
+      if (c < batch)
+        yr[c] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc[q]) + a.bg * a.colsum[c]) : acc[q];
+    }
+  }
+}
+
 // Column sums of x (n x batch, row stride ldx) in fp64, fixed reduction order.
 __global__ void __launch_bounds__(256) k_colsum(const float *__restrict__ x, int64_t n, int64_t ldx, int64_t batch,
                                                 double *__restrict__ out) {
@@ -1494,6 +1648,25 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
   const bool al2 = (ldx % 2 == 0) && (reinterpret_cast<uintptr_t>(x) % 8 == 0);
   const int V = (batch > 64 && al4) ? 4 : ((batch > 32 && al2) ? 2 : 1);
   const int64_t units = a.m * ceil_div(batch, 32 * V);
+  const char *mm_path = getenv("CERDOT_MM_PATH");
+  if (!mm_path || atoi(mm_path) != 0) {
+    // flat entry stream (default); one resident wave of CTAs (occupancy API), units round-robin over warps
+    auto go = [&](auto kern) -> int {
+      static int per_sm = 0;  // per template instance
+      if (per_sm == 0) CERDOT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+      const int grid = static_cast<int>(std::max<int64_t>(
+          1, std::min<int64_t>(ceil_div(units, 8), int64_t(num_sms()) * std::max(per_sm, 1))));
+      kern<<<grid, 256, 0, st>>>(a, x, ldx, batch, y, ldy);
+      CERDOT_LAUNCH_CHECK();
+      return CERDOT_OK;
+    };
+    // measured (tools/mm_time.py): VGG fc6 B=128 (4096 units) 196 us at D=8 vs 231 at D=4; ResNet conv
+    // B=1568 (6656 units) 827 vs ~1200, 32768^2 B=256 22.1 vs 31.7 ms
+    if (V == 4 && units <= int64_t(num_sms()) * 32) return go(k_matmat_flat<ColT, PtrT, CSER, 4, 8>);
+    if (V == 4) return go(k_matmat_flat<ColT, PtrT, CSER, 4, 4>);
+    if (V == 2) return go(k_matmat_flat<ColT, PtrT, CSER, 2, 8>);
+    return go(k_matmat_flat<ColT, PtrT, CSER, 1, 8>);
+  }
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(units, 8),
                                                                            int64_t(num_sms()) * 8)));
   if (V == 4)

@@ -53,7 +53,10 @@ def main():
         batch = int(b)
         cfg = synth.config(name)
         rng = np.random.default_rng(0)
-        w = torch.from_numpy(synth.make_weights(cfg, rng)).cuda()
+        if cfg.m * cfg.n > 10**9:
+            w = synth.make_weights_device(cfg, 0, "cuda")
+        else:
+            w = torch.from_numpy(synth.make_weights(cfg, rng)).cuda()
         x = synth.make_inputs(cfg, rng, batch)
         for kind in ("cer", "cser"):
             enc = (cd.encode_cer if kind == "cer" else cd.encode_cser)(w)
