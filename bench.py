@@ -314,11 +314,13 @@ def measure_case(cd, torch, cfg_name: str, batch: int, steps: int, warmup: int, 
         def step(i):
             cd.dot_device(copies[i], xs[i], out=ys[i])
 
-        secs = _graph_time(step, steps, warmup, rotate, torch)
+        sampler = ClockSampler(torch.cuda.current_device())
+        secs = _graph_time(step, steps, warmup, rotate, torch, sampler)
         t = secs / steps
         out[kind] = {"us": round(t * 1e6, 3), "steps": steps, "alg_bytes": nbytes, "gbs": round(nbytes / t / 1e9, 2),
                      "hbm_frac": round(nbytes / t / 1e9 / peak, 4), "gmacs": round(cfg.m * cfg.n * batch / t / 1e9, 2),
-                     "adds_per_s_T": round(enc.nnz * batch / t / 1e12, 3), "rotating_copies": rotate}
+                     "adds_per_s_T": round(enc.nnz * batch / t / 1e12, 3), "rotating_copies": rotate,
+                     "clocks": sampler.summary()}
         del copies, xs, ys
     del wt
     torch.cuda.empty_cache()

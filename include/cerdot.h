@@ -137,7 +137,8 @@ int cerdot_encode_fill(const cerdot_encode_info *info, int32_t kind, void *works
                        void *stream);
 
 /* Workspace the dot needs (zero unless the background is non-zero: then
- * batch doubles for the column sums of x). */
+ * batch doubles for the column sums of x, plus 16 x batch doubles of
+ * row-range partial sums when batch > 1). */
 size_t cerdot_dot_workspace_bytes(const cerdot_matrix *a, int64_t batch);
 
 /* y (m x batch, row stride ldy) = A . x (n x batch, row stride ldx), fp32.

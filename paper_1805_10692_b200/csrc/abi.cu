@@ -122,7 +122,8 @@ int cerdot_encode_fill(const cerdot_encode_info *info, int32_t kind, void *works
 
 size_t cerdot_dot_workspace_bytes(const cerdot_matrix *a, int64_t batch) {
   if (a == nullptr || a->background == 0.0 || batch <= 0) return 0;
-  return sizeof(double) * static_cast<size_t>(batch);
+  // column sums, plus 16 row-range partials per column for batch > 1 (dot.cu: kColsumSplit)
+  return sizeof(double) * static_cast<size_t>(batch) * (batch > 1 ? 17 : 1);
 }
 
 int cerdot_dot(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,

@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <map>
 #include <set>
 #include <utility>
 #include <string>
@@ -85,6 +86,31 @@ int allow_max_smem(K kern) {
   CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   std::lock_guard<std::mutex> lock(mu);
   done.insert(key);
+  return CERDOT_OK;
+}
+
+// Resident CTAs per SM of a kernel at `threads` threads (no dynamic shared memory), cached per kernel
+// and device.  (Keyed by the kernel's address: every k_matmat_flat instance has the same C++ type.)
+template <typename K>
+int blocks_per_sm(K kern, int threads, int *out) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, int> cache;
+  int dev = 0;
+  CERDOT_CUDA_CHECK(cudaGetDevice(&dev));
+  const auto key = std::make_pair(reinterpret_cast<const void *>(kern), dev);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    const auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return CERDOT_OK;
+    }
+  }
+  int n = 0;
+  CERDOT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, 0));
+  std::lock_guard<std::mutex> lock(mu);
+  cache[key] = n;
+  *out = n;
   return CERDOT_OK;
 }
 
@@ -1397,8 +1423,10 @@ __global__ void __launch_bounds__(256) k_matmat_flat(DotArgs a, const float *__r
                                                                       int64_t ldx, int64_t batch,
                                                                       float *__restrict__ y, int64_t ldy) {
   __shared__ float vtab_all[8][32];
+  __shared__ uint32_t cbuf_all[8][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   float *vtab = vtab_all[wid];
+  const uint32_t *cbuf = cbuf_all[wid];
   const ColT *col = static_cast<const ColT *>(a.col);
   const PtrT *op = static_cast<const PtrT *>(a.op);
   const int64_t chunks = ceil_div(batch, 32 * V);
@@ -1413,8 +1441,13 @@ __global__ void __launch_bounds__(256) k_matmat_flat(DotArgs a, const float *__r
     if (s1 > s0) {
       const float *xb = x + cb;
       const bool full = cb + V <= batch;
+      const bool all_full = __all_sync(0xffffffffu, full);  // no per-load guard (B a multiple of 32 V)
       const int nval = static_cast<int>(max64(0, min64(V, batch - cb)));
-      const uint32_t ldx32 = static_cast<uint32_t>(ldx);
+      const uint32_t ldx_b = static_cast<uint32_t>(ldx) * 4u;  // X row stride in bytes
+      // X row c of this lane's columns: one IMAD.WIDE from a 32-bit index
+      auto xrow = [&](uint32_t c) {
+        return reinterpret_cast<const float *>(reinterpret_cast<const char *>(xb) + static_cast<uint64_t>(c) * ldx_b);
+      };
       const uint32_t e0 = a.re ? __ldg(a.re + row) : ld_idx(op, s0);
       const uint32_t e1 = a.re ? __ldg(a.re + row + 1) : ld_idx(op, s1);
       // segment batch (lane j: segment sb + j) with the next batch prefetched
@@ -1454,18 +1487,20 @@ __global__ void __launch_bounds__(256) k_matmat_flat(DotArgs a, const float *__r
           v = nv;
           fetch(sb + 32, nst, nen, nv);
         }
+        cbuf_all[wid][lane] = cur;  // the chunk's column indices, read back as broadcasts
         __syncwarp();
         const uint32_t cnt = cend - ch;
-        // D X-row loads in flight: 8, or 4 for V = 4 when there are many units (78 instead of 112
-        // registers, 3 CTAs per SM instead of 2)
+        // D X-row loads in flight
         if (cnt == 32) {
 #pragma unroll
           for (int i0 = 0; i0 < 32; i0 += D) {
             float xv[D][V];
+            if (all_full) {
 #pragma unroll
-            for (int i = 0; i < D; ++i) {
-              const uint32_t c = __shfl_sync(0xffffffffu, cur, i0 + i);
-              ld_xrow<V>(xb + static_cast<size_t>(c) * ldx32, full, nval, xv[i]);
+              for (int i = 0; i < D; ++i) ld_xrow<V>(xrow(cbuf[i0 + i]), true, V, xv[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < D; ++i) ld_xrow<V>(xrow(cbuf[i0 + i]), full, nval, xv[i]);
             }
 #pragma unroll
             for (int i = 0; i < D; ++i) {
@@ -1485,10 +1520,8 @@ __global__ void __launch_bounds__(256) k_matmat_flat(DotArgs a, const float *__r
           for (uint32_t i0 = 0; i0 < cnt; i0 += D) {
             float xv[D][V];
 #pragma unroll
-            for (int i = 0; i < D; ++i) {
-              const uint32_t c = __shfl_sync(0xffffffffu, cur, (i0 + i) & 31u);
-              if (i0 + i < cnt) ld_xrow<V>(xb + static_cast<size_t>(c) * ldx32, full, nval, xv[i]);
-            }
+            for (int i = 0; i < D; ++i)
+              if (i0 + i < cnt) ld_xrow<V>(xrow(cbuf[(i0 + i) & 31u]), full, nval, xv[i]);
 #pragma unroll
             for (int i = 0; i < D; ++i) {
               if (i0 + i < cnt) {
@@ -1506,7 +1539,7 @@ __global__ void __launch_bounds__(256) k_matmat_flat(DotArgs a, const float *__r
             }
           }
         }
-        __syncwarp();  // vtab is rewritten for the next chunk
+        __syncwarp();  // vtab and cbuf are rewritten for the next chunk
         cur = nxt;
       }
     }
@@ -1520,26 +1553,30 @@ __global__ void __launch_bounds__(256) k_matmat_flat(DotArgs a, const float *__r
   }
 }
 
-// Column sums of x (n x batch, row stride ldx) in fp64, fixed reduction order.
-__global__ void __launch_bounds__(256) k_colsum(const float *__restrict__ x, int64_t n, int64_t ldx, int64_t batch,
-                                                double *__restrict__ out) {
+// Column sums of x (n x batch, row stride ldx) in fp64, fixed reduction order, in two passes:
+// k_colsum_part sums row range s (of kColsumSplit) of 32 columns per CTA (8 strided partials in flight,
+// combined in order), k_colsum_fin adds the kColsumSplit partials in order.  (One CTA per 32 columns
+// was 49 CTAs for the ResNet conv layer at B = 1568: ~0.1 ms of a ~0.9 ms call with X cold.)
+constexpr int kColsumSplit = 16;
+
+__global__ void __launch_bounds__(256) k_colsum_part(const float *__restrict__ x, int64_t n, int64_t ldx,
+                                                     int64_t batch, double *__restrict__ part_out) {
   __shared__ double part[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + tx;
+  const int64_t r0 = blockIdx.y * n / kColsumSplit, r1 = (blockIdx.y + 1) * n / kColsumSplit;
   double s = 0.0;
   if (c < batch) {
-    // same order as a plain r += 8 loop, but 16 loads in flight (a serial load-add chain cost ~0.25 ms
-    // on the ResNet conv layer at B = 1568)
     constexpr int kU = 16;
-    int64_t r = ty;
-    for (; r + 8 * (kU - 1) < n; r += 8 * kU) {
+    int64_t r = r0 + ty;
+    for (; r + 8 * (kU - 1) < r1; r += 8 * kU) {
       float v[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) v[u] = __ldg(x + (r + 8 * u) * ldx + c);
 #pragma unroll
       for (int u = 0; u < kU; ++u) s += static_cast<double>(v[u]);
     }
-    for (; r < n; r += 8) s += static_cast<double>(__ldg(x + r * ldx + c));
+    for (; r < r1; r += 8) s += static_cast<double>(__ldg(x + r * ldx + c));
   }
   part[ty][tx] = s;
   __syncthreads();
@@ -1547,8 +1584,18 @@ __global__ void __launch_bounds__(256) k_colsum(const float *__restrict__ x, int
     double t = 0.0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) t += part[j][tx];
-    out[c] = t;
+    part_out[blockIdx.y * batch + c] = t;
   }
+}
+
+__global__ void __launch_bounds__(256) k_colsum_fin(const double *__restrict__ part, int64_t batch,
+                                                    double *__restrict__ out) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= batch) return;
+  double t = 0.0;
+#pragma unroll
+  for (int s = 0; s < kColsumSplit; ++s) t += part[s * batch + c];
+  out[c] = t;
 }
 
 // Mat-vec column sum: one CTA tree reduction.
@@ -1652,18 +1699,17 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
   if (!mm_path || atoi(mm_path) != 0) {
     // flat entry stream (default); one resident wave of CTAs (occupancy API), units round-robin over warps
     auto go = [&](auto kern) -> int {
-      static int per_sm = 0;  // per template instance
-      if (per_sm == 0) CERDOT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+      int per_sm = 0;
+      if (int rc_ = blocks_per_sm(kern, 256, &per_sm)) return rc_;
       const int grid = static_cast<int>(std::max<int64_t>(
           1, std::min<int64_t>(ceil_div(units, 8), int64_t(num_sms()) * std::max(per_sm, 1))));
       kern<<<grid, 256, 0, st>>>(a, x, ldx, batch, y, ldy);
       CERDOT_LAUNCH_CHECK();
       return CERDOT_OK;
     };
-    // measured (tools/mm_time.py): VGG fc6 B=128 (4096 units) 196 us at D=8 vs 231 at D=4; ResNet conv
-    // B=1568 (6656 units) 827 vs ~1200, 32768^2 B=256 22.1 vs 31.7 ms
-    if (V == 4 && units <= int64_t(num_sms()) * 32) return go(k_matmat_flat<ColT, PtrT, CSER, 4, 8>);
-    if (V == 4) return go(k_matmat_flat<ColT, PtrT, CSER, 4, 4>);
+    // 8 X-row loads in flight for every V (measured: V = 4 at D = 4 runs 3 CTAs per SM instead of 2
+    // but is slower on all of VGG fc6 B=128, ResNet conv B=1568 and 32768^2 B=256)
+    if (V == 4) return go(k_matmat_flat<ColT, PtrT, CSER, 4, 8>);
     if (V == 2) return go(k_matmat_flat<ColT, PtrT, CSER, 2, 8>);
     return go(k_matmat_flat<ColT, PtrT, CSER, 1, 8>);
   }
@@ -1754,10 +1800,15 @@ int dot(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, fl
     if (workspace == nullptr || workspace_bytes < sizeof(double) * static_cast<size_t>(batch))
       return fail(CERDOT_E_WORKSPACE, "dot workspace too small for the background column sums");
     double *cs = static_cast<double *>(workspace);
-    if (batch == 1)
+    if (batch == 1) {
       k_vecsum<<<1, 1024, 0, st>>>(x, a.n, cs);
-    else
-      k_colsum<<<static_cast<int>(ceil_div(batch, 32)), 256, 0, st>>>(x, a.n, ldx, batch, cs);
+    } else {
+      if (workspace_bytes < sizeof(double) * static_cast<size_t>(batch) * (1 + kColsumSplit))
+        return fail(CERDOT_E_WORKSPACE, "dot workspace too small for the background column sums");
+      k_colsum_part<<<dim3(static_cast<unsigned>(ceil_div(batch, 32)), kColsumSplit), 256, 0, st>>>(
+          x, a.n, ldx, batch, cs + batch);
+      k_colsum_fin<<<static_cast<unsigned>(ceil_div(batch, 256)), 256, 0, st>>>(cs + batch, batch, cs);
+    }
     CERDOT_LAUNCH_CHECK();
     a.colsum = cs;
   }

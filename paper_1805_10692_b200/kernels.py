@@ -219,7 +219,8 @@ def dot_device(enc, x, out=None, stream=None):
         out = torch.empty((dev.m,) if batch == 1 else (dev.m, batch), dtype=torch.float32, device=x.device)
     ldy = 1 if out.ndim == 1 else out.stride(0)
     st = dev.struct()
-    ws_bytes = 8 * batch if dev.background != 0.0 else 0  # cerdot_dot_workspace_bytes
+    # == cerdot_dot_workspace_bytes: the column sums (+ 16 row-range partials each when batch > 1)
+    ws_bytes = (8 * batch * (17 if batch > 1 else 1)) if dev.background != 0.0 else 0
     ws_ptr = _WS.get(x.device, ws_bytes).data_ptr() if ws_bytes else None
     sp = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
     _native.check(_native.lib().cerdot_dot(st, x.data_ptr(), ldx, batch, out.data_ptr(), ldy, ws_ptr, ws_bytes, sp))

@@ -152,6 +152,22 @@ def test_full_batch_resnet_conv_properties():
     assert rel_err(y[:, 1500:].cpu().numpy(), ref) <= REL_TOL
 
 
+@pytest.mark.parametrize("name,batch", [("alexnet-fc6", 64), ("vgg-fc6", 96), ("resnet-conv", 200), ("oracle", 37)])
+def test_matmat_kernels_agree_bitwise(monkeypatch, name, batch):
+    """The flat entry-stream mat-mat kernel and the per-segment one compute every column in the same
+    fp32 order: identical outputs (V = 1, 2, 4; full and partial column chunks; CER and CSER)."""
+    w, _ = synth.make_layer(name)
+    x = torch.from_numpy(np.random.default_rng(2).standard_normal((w.shape[1], batch), dtype=np.float32)).cuda()
+    wt = torch.from_numpy(w).cuda()
+    for encode in (cd.encode_cer, cd.encode_cser):
+        enc = encode(wt)
+        monkeypatch.setenv("CERDOT_MM_PATH", "0")
+        y0 = cd.dot(enc, x)
+        monkeypatch.delenv("CERDOT_MM_PATH")
+        y1 = cd.dot(enc, x)
+        assert torch.equal(y0, y1), (name, encode.__name__)
+
+
 def test_long_rows_default_to_run_kernel_and_match_oracle():
     """Rows of >= 4096 entries take the run kernel by default (colI ring across rows, segment batches
     that close several times inside one window, CER padding); integer alphabet -> bitwise, real -> 1e-5."""

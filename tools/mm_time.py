@@ -60,7 +60,7 @@ def main():
         x = synth.make_inputs(cfg, rng, batch)
         for kind in ("cer", "cser"):
             enc = (cd.encode_cer if kind == "cer" else cd.encode_cser)(w)
-            R = 4
+            R = int(os.environ.get("MM_R", "4"))
             copies = [bench._clone(cd, enc) for _ in range(R)]
             xs = [torch.from_numpy(x).cuda() for _ in range(R)]
             ref = None
