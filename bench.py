@@ -288,7 +288,8 @@ class _Null:
         return False
 
 
-def measure_case(cd, torch, cfg_name: str, batch: int, steps: int, warmup: int, seed: int, device):
+def measure_case(cd, torch, cfg_name: str, batch: int, steps: int, warmup: int, seed: int, device,
+                 library_baselines: bool = True):
     """One config x batch: CER and CSER dot timed separately (graphs, rotating cold copies)."""
     from paper_1805_10692_b200 import synth
 
@@ -322,9 +323,73 @@ def measure_case(cd, torch, cfg_name: str, batch: int, steps: int, warmup: int, 
                      "adds_per_s_T": round(enc.nnz * batch / t / 1e12, 3), "rotating_copies": rotate,
                      "clocks": sampler.summary()}
         del copies, xs, ys
+    if library_baselines:
+        out["library_baselines"] = library_baseline_times(torch, wt, x, device)
     del wt
     torch.cuda.empty_cache()
     return out
+
+
+def _eager_time(fn, calls: int, warmup: int, torch) -> float:
+    """Seconds per call of fn(i) (eager launches, CUDA events, rotating operands)."""
+    for i in range(warmup):
+        fn(i)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for i in range(calls):
+        fn(i)
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / 1e3 / calls
+
+
+def library_baseline_times(torch, wt, x_np, device, budget_s: float = 0.05) -> dict:
+    """The same product through the vendor libraries on the same matrix (the
+    paper's entropy-format-vs-sparse-vs-dense comparison, on B200): cuSPARSE CSR SpMV/SpMM (torch CSR,
+    int32 indices, fp32 values) and cuBLAS fp32 GEMV/GEMM on the dense W (TF32 off).  Rotating copies
+    of the operands above L2 size, eager launches, CUDA events.  Comparison only; not the product path."""
+    m, n = wt.shape
+    batch = 1 if x_np.ndim == 1 else x_np.shape[1]
+    res = {}
+    prev_tf32 = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        x = torch.from_numpy(x_np).to(device)
+        x2 = x.reshape(n, batch)
+        # cuBLAS dense (W fp32 row-major, m x n)
+        dense_bytes = wt.numel() * 4
+        rot = max(1, min(4, -(-2 * L2_BYTES // dense_bytes)))
+        if rot * dense_bytes < 40 * 2**30:
+            ws = [wt] + [wt.clone() for _ in range(rot - 1)]
+            ys = [torch.empty((m, batch), device=device) for _ in range(rot)]
+            t1 = _eager_time(lambda i: torch.matmul(ws[i % rot], x2, out=ys[i % rot]), 1, 2, torch)
+            calls = max(3, min(2000, int(budget_s / max(t1, 1e-6))))
+            t = _eager_time(lambda i: torch.matmul(ws[i % rot], x2, out=ys[i % rot]), calls, 3, torch)
+            res["cublas_dense_fp32"] = {"us": round(t * 1e6, 3), "bytes": dense_bytes + 4 * (n + m) * batch,
+                                        "gbs": round((dense_bytes + 4 * (n + m) * batch) / t / 1e9, 2)}
+            del ws, ys
+        # cuSPARSE CSR (int32 indices)
+        csr = wt.to_sparse_csr()
+        crow, col, val = csr.crow_indices().int(), csr.col_indices().int(), csr.values()
+        del csr
+        csr_bytes = val.numel() * 8 + crow.numel() * 4
+        rot = max(1, min(4, -(-2 * L2_BYTES // max(1, csr_bytes))))
+        mats = [torch.sparse_csr_tensor(crow.clone() if i else crow, col.clone() if i else col,
+                                        val.clone() if i else val, size=(m, n), check_invariants=False)
+                for i in range(rot)]
+        t1 = _eager_time(lambda i: torch.matmul(mats[i % rot], x2), 1, 2, torch)
+        calls = max(3, min(2000, int(budget_s / max(t1, 1e-6))))
+        t = _eager_time(lambda i: torch.matmul(mats[i % rot], x2), calls, 3, torch)
+        res["cusparse_csr_fp32"] = {"us": round(t * 1e6, 3), "bytes": csr_bytes + 4 * (n + m) * batch,
+                                    "gbs": round((csr_bytes + 4 * (n + m) * batch) / t / 1e9, 2),
+                                    "index": "int32"}
+        del mats, crow, col, val
+    except Exception as ex:  # pragma: no cover - reported, never fatal
+        res["error"] = repr(ex)[:200]
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev_tf32
+    return res
 
 
 def _clone(cd, enc):
@@ -446,6 +511,7 @@ def run_ours(args):
                 if name == "large":
                     steps_c = 20 if b == 1 else 3
                 cases.append(measure_case(cd, torch, name, b, steps_c, 3, args.seed, device))
+        libs = library_baseline_times(torch, wt, x_host, device) if (args.cases == "all" and world == 1) else {}
         fmt_b = {"cer": cd.storage_bits(cer) // 8, "cser": cd.storage_bits(cser) // 8}
         traffic = _ncu_traffic(cfg.name)
         result = {
@@ -494,6 +560,7 @@ def run_ours(args):
                            "dense_input_gbs": round(w.nbytes / t_enc_cer / 1e9, 2)},
             "clocks": clocks,
             "gpu_launches": 2 * args.steps,
+            "library_baselines": libs,
             "cases": cases,
         }
         print(json.dumps(result), flush=True)
