@@ -86,20 +86,42 @@ class RowShardedDot:
         self._gather = None
 
     def __call__(self, x):
+        return self.start(x).wait()
+
+    def start(self, x) -> "PendingRows":
+        """Compute the local block and start the all-gather without waiting for it: work queued on the
+        current stream afterwards (e.g. the next layer's local dot) overlaps the exchange.  ``wait()``
+        on the result returns the full y (the current stream then waits for the collective)."""
         import torch
         import torch.distributed as dist
 
         y = self.compute(self.local, x)
         if self.world == 1:
-            return y
+            return PendingRows(y, None, None)
         shape = (self.block,) + tuple(y.shape[1:])
         if y.shape[0] != self.block:
             pad = torch.zeros(shape, dtype=y.dtype, device=y.device)
             pad[: y.shape[0]] = y
             y = pad
         out = torch.empty((self.world * self.block,) + tuple(y.shape[1:]), dtype=y.dtype, device=y.device)
-        dist.all_gather_into_tensor(out, y.contiguous(), group=self.group)
-        if all(r == self.block for r in self.rows):
-            return out
-        parts = [out[i * self.block: i * self.block + r] for i, r in enumerate(self.rows)]
-        return torch.cat(parts, dim=0)
+        work = dist.all_gather_into_tensor(out, y.contiguous(), group=self.group, async_op=True)
+        rows = None if all(r == self.block for r in self.rows) else (self.block, self.rows)
+        return PendingRows(out, work, rows)
+
+
+class PendingRows:
+    """An in-flight row-sharded product (RowShardedDot.start)."""
+
+    def __init__(self, out, work, rows):
+        self._out, self._work, self._rows = out, work, rows
+
+    def wait(self):
+        import torch
+
+        if self._work is not None:
+            self._work.wait()
+            self._work = None
+        if self._rows is None:
+            return self._out
+        block, rows = self._rows
+        return torch.cat([self._out[i * block: i * block + r] for i, r in enumerate(rows)], dim=0)

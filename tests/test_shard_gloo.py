@@ -59,6 +59,38 @@ def _worker(rank, world, port, kind, balanced, result_path):
         dist.destroy_process_group()
 
 
+def _worker_overlap(rank, world, port, result_path):
+    """CER and CSER products started back to back (two all-gathers in flight), then waited."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w, xs = synth.make_layer("oracle")
+        ops = []
+        for kind in ("cer", "cser"):
+            full = _host_encoding(kind, w)
+            bounds = shard.plan_rows(full, world)
+            local = shard.slice_rows(full, bounds[rank], bounds[rank + 1])
+            ops.append(shard.RowShardedDot(local, [bounds[i + 1] - bounds[i] for i in range(world)],
+                                           compute=_oracle_compute))
+        x = torch.from_numpy(xs[1].astype(np.float64))
+        pending = [op.start(x) for op in ops]
+        ys = [p.wait() for p in pending]
+        if rank == 0:
+            np.save(result_path, np.stack([y.numpy() for y in ys]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_overlapped_products_world2(tmp_path):
+    out = str(tmp_path / "y2.npy")
+    mp.spawn(_worker_overlap, args=(2, _free_port(), out), nprocs=2, join=True)
+    w, xs = synth.make_layer("oracle")
+    got = np.load(out)
+    for i, kind in enumerate(("cer", "cser")):
+        assert np.array_equal(got[i], c_oracle.dot(_as_dict(_host_encoding(kind, w)), xs[1].astype(np.float64)))
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
