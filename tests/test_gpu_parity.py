@@ -168,6 +168,22 @@ def test_matmat_kernels_agree_bitwise(monkeypatch, name, batch):
         assert torch.equal(y0, y1), (name, encode.__name__)
 
 
+@pytest.mark.parametrize("path", ["1", "2", "3"])
+def test_u32_column_indices(monkeypatch, path):
+    """n > 65535 (u32 colI): every mat-vec kernel and the mat-mat kernel, integer alphabet -> bitwise."""
+    monkeypatch.setenv("CERDOT_MATVEC_PATH", path)
+    rng = np.random.default_rng(31)
+    m, n = 40, 70001
+    w = rng.choice(np.arange(-3.0, 4.0), size=(m, n), p=[0.02, 0.03, 0.05, 0.8, 0.05, 0.03, 0.02])
+    w[3] = 0.0
+    x = rng.integers(-2, 3, size=(n, 5)).astype(np.float64)
+    for encode in (cd.encode_cer, cd.encode_cser):
+        enc = encode(w)
+        assert enc.col_index_bits == 32
+        assert np.array_equal(cd.dot(enc, x[:, 0]), w @ x[:, 0]), encode.__name__
+        assert np.array_equal(cd.dot(enc, x), w @ x), encode.__name__
+
+
 def test_long_rows_default_to_run_kernel_and_match_oracle():
     """Rows of >= 4096 entries take the run kernel by default (colI ring across rows, segment batches
     that close several times inside one window, CER padding); integer alphabet -> bitwise, real -> 1e-5."""
