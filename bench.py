@@ -448,14 +448,27 @@ def run_ours(args):
 
         secs = _graph_time(step, args.steps, args.warmup, rotate, torch, sampler)
     else:
-        shard_cer = [RowShardedDot(c, rows) for c in cers]
-        shard_cser = [RowShardedDot(c, rows) for c in csers]
-        def sharded_step(i):
-            # the CSER block's kernel runs while the CER block's y is being all-gathered
-            p_cer = shard_cer[i % rotate].start(xdev[i % rotate])
-            p_cser = shard_cser[i % rotate].start(xdev[i % rotate])
-            p_cer.wait()
-            p_cser.wait()
+        try:  # y all-gather fused into the kernels' epilogue (NVLink peer stores), one barrier per step
+            from paper_1805_10692_b200.shard import PeerRowShardedDot
+
+            shard_cer = [PeerRowShardedDot(c, rows, batch=1) for c in cers]
+            shard_cser = [PeerRowShardedDot(c, rows, batch=1) for c in csers]
+            exchange = "fused: cerdot_dot_peers epilogue stores to every rank's symmetric-memory buffer + one barrier"
+
+            def sharded_step(i):
+                shard_cer[i % rotate](xdev[i % rotate], barrier=False)
+                shard_cser[i % rotate](xdev[i % rotate])
+        except Exception as ex:  # symmetric memory unavailable: NCCL all-gather, left in flight
+            shard_cer = [RowShardedDot(c, rows) for c in cers]
+            shard_cser = [RowShardedDot(c, rows) for c in csers]
+            exchange = f"NCCL all_gather_into_tensor, async (symmetric memory unavailable: {type(ex).__name__})"
+
+            def sharded_step(i):
+                # the CSER block's kernel runs while the CER block's y is being all-gathered
+                p_cer = shard_cer[i % rotate].start(xdev[i % rotate])
+                p_cser = shard_cser[i % rotate].start(xdev[i % rotate])
+                p_cer.wait()
+                p_cser.wait()
 
         for i in range(max(args.warmup, 3)):
             sharded_step(i)
@@ -540,6 +553,7 @@ def run_ours(args):
                 "alg_bytes_per_step": step_bytes,
                 "format_bytes": fmt_b,
                 "parallelism": f"rows x{world} (all-gather of y)" if world > 1 else "single GPU",
+                "exchange": exchange if world > 1 else None,
                 "timing": "CUDA graphs of rotating steps, CUDA events around exactly K steps" if world == 1
                           else "eager, CUDA events, max over ranks",
             },

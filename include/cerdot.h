@@ -150,6 +150,17 @@ int cerdot_dot_cer(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t 
 int cerdot_dot_cser(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,
                     void *workspace, size_t workspace_bytes, void *stream);
 
+/* Row-sharded dot with the output all-gather fused into the kernels' epilogue: this
+ * rank's block y (rows of its shard) is written to `y` as by cerdot_dot and, element by element, to
+ * position peer_offset + i of each of the `npeers` other ranks' full-output buffers (`peers`: a DEVICE
+ * array of device pointers, e.g. the NVLink peer mappings of a symmetric-memory buffer; peer_offset =
+ * the shard's first row times ldy).  The stores leave from the epilogue as each row finishes, so the
+ * exchange overlaps the rest of the computation.  The caller completes it with a stream-ordered
+ * cross-rank barrier (signal/wait) after the call.  npeers = 0 is cerdot_dot. */
+int cerdot_dot_peers(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,
+                     float *const *peers, int32_t npeers, int64_t peer_offset, void *workspace,
+                     size_t workspace_bytes, void *stream);
+
 /* Host-buffer convenience (the e2e path of the reference-facing API): copies x (HOST, fp32, n x batch,
  * row stride ldx; pinned for asynchronous copies) to the device, runs cerdot_dot, copies y (HOST,
  * m x batch, row stride ldy) back and synchronises `stream`.  The device workspace (size from

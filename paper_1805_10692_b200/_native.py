@@ -80,6 +80,8 @@ _SIGNATURES = {
                                           _P, _I32, _P, _I32, _P]),
     "cerdot_dot_workspace_bytes": (_SZ, [ctypes.POINTER(CerdotMatrix), _I64]),
     "cerdot_dot": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _SZ, _P]),
+    "cerdot_dot_peers": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _I32, _I64, _P,
+                                        _SZ, _P]),
     "cerdot_dot_cer": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _SZ, _P]),
     "cerdot_dot_cser": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _SZ, _P]),
     "cerdot_dot_host_workspace_bytes": (_SZ, [ctypes.POINTER(CerdotMatrix), _I64]),

@@ -126,6 +126,17 @@ size_t cerdot_dot_workspace_bytes(const cerdot_matrix *a, int64_t batch) {
   return sizeof(double) * static_cast<size_t>(batch) * (batch > 1 ? 17 : 1);
 }
 
+int cerdot_dot_peers(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,
+                     float *const *peers, int32_t npeers, int64_t peer_offset, void *workspace,
+                     size_t workspace_bytes, void *stream) {
+  int rc = check_matrix(a, batch, x, y, ldx, ldy);
+  if (rc) return rc;
+  if (npeers < 0 || (npeers > 0 && peers == nullptr) || peer_offset < 0)
+    return fail(CERDOT_E_VALUE, "dot_peers: need a device array of npeers >= 0 peer output pointers");
+  return cerdot::dot(a, x, ldx, batch, y, ldy, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), peers,
+                     npeers, peer_offset);
+}
+
 int cerdot_dot(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,
                void *workspace, size_t workspace_bytes, void *stream) {
   int rc = check_matrix(a, batch, x, y, ldx, ldy);

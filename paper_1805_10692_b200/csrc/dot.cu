@@ -69,7 +69,18 @@ struct DotArgs {
   int64_t max_row_nnz, max_row_segs;
   const uint32_t *re;  // optional row_entry index (m+1): re[r] = op[rp[r]]
   int dbg;  // CERDOT_TRACE: print per-CTA phase timestamps (debug only)
+  // fused output exchange (cerdot_dot_peers): every y element is also stored at ypeer_off + i of each
+  // peer's output buffer (NVLink P2P stores); npeer = 0 for a plain dot
+  float *const *ypeer;
+  int npeer;
+  int64_t ypeer_off;
 };
+
+// y[i] = v, and the same element of every peer's output (the row-sharded all-gather, fused).
+__device__ __forceinline__ void put_y(const DotArgs &a, float *y, int64_t i, float v) {
+  y[i] = v;
+  for (int p = 0; p < a.npeer; ++p) a.ypeer[p][a.ypeer_off + i] = v;
+}
 
 // Raise a kernel's dynamic shared-memory limit once per kernel (and device) -- the host call costs ~us.
 template <typename K>
@@ -491,7 +502,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
   float acc = 0.f, carry = 0.f;
   uint32_t sc = 0;
   auto emit_empty = [&](uint32_t upto) {
-    for (uint32_t r = next_emit + lane; r < upto; r += 32) y[r] = y_empty;
+    for (uint32_t r = next_emit + lane; r < upto; r += 32) put_y(a, y, r, y_empty);
     next_emit = max(next_emit, upto);
   };
   auto process = [&](const uint4 *cur, const Win &w) {
@@ -625,7 +636,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
       float r = acc;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-      if (lane == 0) y[w.row] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(r) + a.bg * a.colsum[0]) : r;
+      if (lane == 0) put_y(a, y, w.row, a.bg != 0.0 ? static_cast<float>(static_cast<double>(r) + a.bg * a.colsum[0]) : r);
       next_emit = w.row + 1;
     }
   };
@@ -909,8 +920,8 @@ __global__ void __launch_bounds__(kTileNT, 1) k_matvec_tile(DotArgs a, const flo
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0)
-          y[g0 + r] = s1 > s0 ? (a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + a.bg * a.colsum[0]) : acc)
-                              : y_empty;
+          put_y(a, y, g0 + r, s1 > s0 ? (a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + a.bg * a.colsum[0]) : acc)
+                              : y_empty);
       }
       __syncthreads();  // stage (u % 2), the prefix table and scans are free again
       if (tid == 0 && t + 2 < nt) issue(trow[t + 2], trow[t + 3], issued++);
@@ -1217,7 +1228,7 @@ __global__ void __launch_bounds__(kRunNT, 1) k_matvec_run(DotArgs a, const float
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) y[r] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + a.bg * a.colsum[0]) : acc;
+    if (lane == 0) put_y(a, y, r, a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + a.bg * a.colsum[0]) : acc);
   }
   if (!x_ready) mbar_wait(xbar, 0);  // no CTA exits with a bulk copy in flight
   cp_async_wait<0>();
@@ -1265,7 +1276,7 @@ __global__ void __launch_bounds__(256) k_matvec_generic(DotArgs a, const float *
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) y[row] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + a.bg * a.colsum[0]) : acc;
+    if (lane == 0) put_y(a, y, row, a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + a.bg * a.colsum[0]) : acc);
   }
 }
 
@@ -1382,12 +1393,12 @@ __global__ void __launch_bounds__(256, (V == 4 ? 4 : 1)) k_matmat(DotArgs a, con
         }
       }
     }
-    float *yr = y + row * ldy;
 #pragma unroll
     for (int q = 0; q < V; ++q) {
       const int64_t c = cb + q;
       if (c < batch)
-        yr[c] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc[q]) + a.bg * a.colsum[c]) : acc[q];
+        put_y(a, y, row * ldy + c,
+              a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc[q]) + a.bg * a.colsum[c]) : acc[q]);
     }
   }
 }
@@ -1543,12 +1554,12 @@ __global__ void __launch_bounds__(256) k_matmat_flat(DotArgs a, const float *__r
         cur = nxt;
       }
     }
-    float *yr = y + row * ldy;
 #pragma unroll
     for (int q = 0; q < V; ++q) {
       const int64_t c = cb + q;
       if (c < batch)
-        yr[c] = a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc[q]) + a.bg * a.colsum[c]) : acc[q];
+        put_y(a, y, row * ldy + c,
+              a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc[q]) + a.bg * a.colsum[c]) : acc[q]);
     }
   }
 }
@@ -1775,9 +1786,12 @@ int row_entries(const cerdot_matrix *mat, uint32_t *out, cudaStream_t st) {
 }
 
 int dot(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy, void *workspace,
-        size_t workspace_bytes, cudaStream_t st) {
+        size_t workspace_bytes, cudaStream_t st, float *const *peers, int npeers, int64_t peer_offset) {
   const bool cser = mat->kind == CERDOT_CSER;
   DotArgs a{};
+  a.ypeer = peers;
+  a.npeer = peers ? npeers : 0;
+  a.ypeer_off = peer_offset;
   a.omega = mat->omega;
   a.col = mat->col_index;
   a.op = mat->omega_ptr;

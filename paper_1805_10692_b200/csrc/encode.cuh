@@ -23,6 +23,7 @@ int encode_sort_fill(const cerdot_encode_info *info, int kind, void *workspace, 
 
 int row_entries(const cerdot_matrix *a, uint32_t *out, cudaStream_t st);
 int dot(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy, void *workspace,
-        size_t workspace_bytes, cudaStream_t st);
+        size_t workspace_bytes, cudaStream_t st, float *const *peers = nullptr, int npeers = 0,
+        int64_t peer_offset = 0);
 
 }  // namespace cerdot

@@ -196,10 +196,13 @@ _WS = _Workspace()
 
 
 
-def dot_device(enc, x, out=None, stream=None):
+def dot_device(enc, x, out=None, stream=None, peers=None, peer_offset: int = 0):
     """Device-only entry: ``x`` a CUDA fp32 tensor (n,) or (n, B); returns y (m,) / (m, B) fp32.
 
-    Stream-ordered on ``stream`` (default: torch's current stream), no host sync.
+    Stream-ordered on ``stream`` (default: torch's current stream), no host sync.  ``peers``: a CUDA
+    int64 tensor of other ranks' output-buffer addresses; every y element is then also stored at element
+    ``peer_offset + i`` of each of them from the kernels' epilogue (cerdot_dot_peers, the fused
+    row-sharded all-gather; the caller adds the cross-rank barrier).
     """
     torch = torch_mod()
     dev = enc._dev if enc._dev is not None else enc.device_encoding(x.device)
@@ -223,6 +226,13 @@ def dot_device(enc, x, out=None, stream=None):
     ws_bytes = (8 * batch * (17 if batch > 1 else 1)) if dev.background != 0.0 else 0
     ws_ptr = _WS.get(x.device, ws_bytes).data_ptr() if ws_bytes else None
     sp = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
+    if peers is not None and peers.numel() > 0:
+        if peers.dtype != torch.int64 or peers.device != x.device:
+            raise ValueError("peers must be an int64 tensor of device pointers on the dot's device")
+        _native.check(_native.lib().cerdot_dot_peers(st, x.data_ptr(), ldx, batch, out.data_ptr(), ldy,
+                                                      peers.data_ptr(), int(peers.numel()), int(peer_offset),
+                                                      ws_ptr, ws_bytes, sp))
+        return out
     _native.check(_native.lib().cerdot_dot(st, x.data_ptr(), ldx, batch, out.data_ptr(), ldy, ws_ptr, ws_bytes, sp))
     return out
 

@@ -9,9 +9,17 @@ block ``[r0, r1)`` cut out of the global encoding (not a re-encode) —
 * ``omega`` unchanged (CER ranks are row-relative, CSER indices global).
 
 The activations are replicated, each rank computes its block of y, and the
-only exchange is one all-gather of the y blocks (NCCL over NVLink on a GPU
-node; gloo in the CPU tests).  Block boundaries come from
-``cerdot_shard_plan`` (balanced encoded bytes).
+only exchange is one all-gather of the y blocks.  Two exchanges:
+
+* ``RowShardedDot``: the local dot, then ``all_gather_into_tensor`` (NCCL over
+  NVLink on a GPU node; gloo in the CPU tests), optionally left in flight
+  (``start``/``wait``) so the next product's kernel overlaps it;
+* ``PeerRowShardedDot``: the all-gather fused into the dot kernels' epilogue
+  (``cerdot_dot_peers``): every finished y element is stored straight into
+  every rank's output buffer over NVLink peer mappings of a torch
+  symmetric-memory buffer, then one stream-ordered signal/wait barrier.
+
+Block boundaries come from ``cerdot_shard_plan`` (balanced encoded bytes).
 """
 
 from __future__ import annotations
@@ -125,3 +133,54 @@ class PendingRows:
             return self._out
         block, rows = self._rows
         return torch.cat([self._out[i * block: i * block + r] for i, r in enumerate(rows)], dim=0)
+
+
+class PeerRowShardedDot:
+    """y = A.x with A's rows split over the ranks, the y all-gather fused into the kernels (NVLink P2P).
+
+    The output lives in a symmetric-memory buffer (``torch.distributed._symmetric_memory``) of
+    world x block rows; the local dot writes its rows into its own block and, from the same epilogue
+    stores, into the same rows of every peer's buffer (``cerdot_dot_peers``).  ``handle.barrier()``
+    (stream-ordered signal/wait over the symmetric signal pads) then makes every rank's copy complete.
+    The returned tensor is the symmetric buffer itself (rows of every rank), valid until the next call
+    on ANY rank (peers write into it): consume or copy it before the ranks' next product, or rotate
+    several instances (as bench.py does).
+    """
+
+    def __init__(self, local, rows_per_rank: list[int], batch: int = 1, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.local = local
+        self.rows = list(rows_per_rank)
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        if len(self.rows) != self.world:
+            raise ValueError(f"{len(self.rows)} row blocks for a world of {self.world}")
+        self.block = max(self.rows)
+        self.batch = int(batch)
+        device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        shape = (self.world * self.block,) if self.batch == 1 else (self.world * self.block, self.batch)
+        self.buf = symm_mem.empty(shape, dtype=torch.float32, device=device)
+        self.handle = symm_mem.rendezvous(self.buf, self.group)
+        ptrs = [int(p) for i, p in enumerate(self.handle.buffer_ptrs) if i != self.rank]
+        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=device)
+        r0 = self.rank * self.block
+        self.y_local = self.buf[r0: r0 + self.rows[self.rank]]
+        self.peer_offset = r0 * (1 if self.batch == 1 else self.batch)
+
+    def __call__(self, x, barrier: bool = True):
+        """``barrier=False`` leaves the exchange to a later call's barrier (one barrier after several
+        products makes all of them complete: it orders every prior peer store of every rank)."""
+        import torch
+
+        from .kernels import dot_device
+
+        dot_device(self.local, x, out=self.y_local, peers=self.peers, peer_offset=self.peer_offset)
+        if barrier:
+            self.handle.barrier(channel=0)
+        if all(r == self.block for r in self.rows):
+            return self.buf
+        return torch.cat([self.buf[i * self.block: i * self.block + r] for i, r in enumerate(self.rows)], dim=0)

@@ -415,3 +415,62 @@ def test_host_buffer_raw_abi_pageable_and_pinned():
         py.zero_()
         _native.check(L.cerdot_dot_host(st, px.data_ptr(), 1, 1, py.data_ptr(), 1, ws.data_ptr(), ws_bytes, stream))
         assert np.array_equal(py.numpy(), y_ref)
+
+
+@pytest.mark.parametrize("name,batch", [("alexnet-fc6", 1), ("resnet-conv", 1), ("alexnet-fc6", 16),
+                                        ("resnet-conv", 40)])
+def test_fused_peer_exchange_emulated_ranks(name, batch):
+    """cerdot_dot_peers, ranks emulated on one GPU (each rank's kernel runs alone; no cross-rank wait):
+    rank r's shard writes its rows into its own buffer and, from the epilogue, into every other rank's
+    buffer.  Afterwards all buffers hold the full product (identical), within the bar of the oracle."""
+    from paper_1805_10692_b200 import shard
+
+    w, _ = synth.make_layer(name)
+    rng = np.random.default_rng(4)
+    xn = rng.standard_normal((w.shape[1], batch) if batch > 1 else w.shape[1], dtype=np.float32)
+    x = torch.from_numpy(xn).cuda()
+    ranks = 3
+    for kind in ("cer", "cser"):
+        full = (cd.encode_cer if kind == "cer" else cd.encode_cser)(torch.from_numpy(w).cuda())
+        bounds = shard.plan_rows(full, ranks)
+        shape = (full.m,) if batch == 1 else (full.m, batch)
+        bufs = [torch.full(shape, float("nan"), device="cuda") for _ in range(ranks)]
+        for r in range(ranks):
+            local = shard.slice_rows(full, bounds[r], bounds[r + 1])
+            peers = torch.tensor([b.data_ptr() for p, b in enumerate(bufs) if p != r], dtype=torch.int64,
+                                 device="cuda")
+            off = bounds[r] * (1 if batch == 1 else batch)
+            cd.dot_device(local, x, out=bufs[r][bounds[r]:bounds[r + 1]], peers=peers, peer_offset=off)
+        torch.cuda.synchronize()
+        for b in bufs[1:]:
+            assert torch.equal(b, bufs[0]), (name, kind)
+        ref = c_oracle.dot(c_oracle.encode(w, kind), xn.astype(np.float64))
+        assert rel_err(bufs[0].cpu().numpy(), ref) <= REL_TOL, (name, kind)
+
+
+def test_peer_row_sharded_dot_single_rank():
+    """PeerRowShardedDot end to end (symmetric memory, barrier) in a one-rank NCCL group."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1805_10692_b200 import shard
+
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        w, xs = synth.make_layer("alexnet-fc6")
+        enc = cd.encode_cer(torch.from_numpy(w).cuda())
+        op = shard.PeerRowShardedDot(enc, [enc.m], batch=1)
+        x = torch.from_numpy(xs[1]).cuda()
+        y = op(x)
+        torch.cuda.synchronize()
+        assert torch.equal(y, cd.dot_device(enc, x))
+    finally:
+        dist.destroy_process_group()
