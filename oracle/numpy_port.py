@@ -216,3 +216,123 @@ def dot_threaded(enc: dict, x, threads: int | None = None) -> np.ndarray:
     with ThreadPoolExecutor(max_workers=threads) as pool:
         parts = list(pool.map(lambda blk: dot(blk, x), blocks))
     return np.concatenate(parts, axis=0)
+
+
+# --------------------------------------------------------------------------- validate / decode
+# Restatement of lemt.formats.validate / decode for CER and CSER (formats.py:298-392, 395-424): the
+# checks run in the reference's order and the first violation is returned as (array, offset, reason)
+# -- the fields of lemt.formats.FormatError -- or None for a valid encoding.
+
+
+def _first_monotone_violation(name: str, arr: np.ndarray, first: int, last: int):
+    """formats.py:298-308: non-empty, starts at `first`, non-decreasing, ends at `last`."""
+    if arr.size == 0:
+        return (name, 0, "array is empty")
+    if int(arr[0]) != first:
+        return (name, 0, f"must start at {first}, found {int(arr[0])}")
+    steps = np.diff(arr.astype(np.int64))
+    down = np.flatnonzero(steps < 0)
+    if down.size:
+        return (name, int(down[0]) + 1, "must be non-decreasing")
+    if int(arr[-1]) != last:
+        return (name, arr.size - 1, f"must end at {last}, found {int(arr[-1])}")
+    return None
+
+
+def _first_duplicate(keys: np.ndarray):
+    """Index of the second occurrence (stable order) of the smallest duplicated key, or None."""
+    order = np.argsort(keys, kind="stable")
+    same = np.flatnonzero(np.diff(keys[order]) == 0)
+    return int(order[same[0] + 1]) if same.size else None
+
+
+def _first_column_violation(cols: np.ndarray, seg_ptr: np.ndarray, n: int, entry_row: np.ndarray):
+    """formats.py:311-329: in range, strictly ascending inside a segment, unique within a row."""
+    c = cols.astype(np.int64)
+    oob = np.flatnonzero(c >= n)
+    if oob.size:
+        return ("colI", int(oob[0]), f"column {int(c[oob[0]])} out of range for n={n}")
+    if c.size > 1:
+        seg_start = np.zeros(c.size, dtype=bool)
+        heads = seg_ptr[:-1].astype(np.int64)
+        seg_start[heads[heads < c.size]] = True
+        bad = np.flatnonzero((np.diff(c) <= 0) & ~seg_start[1:])
+        if bad.size:
+            return ("colI", int(bad[0]) + 1, "must be strictly ascending within a segment")
+    dup = _first_duplicate(entry_row.astype(np.int64) * n + c)
+    if dup is not None:
+        return ("colI", dup, "duplicate column within a row")
+    return None
+
+
+def validate(enc: dict):
+    """First structural violation of a CER/CSER encoding (dict as produced by encode_cer/encode_cser)."""
+    omega = np.asarray(enc["omega"], dtype=np.float64)
+    op, rp, col = (np.asarray(enc[k]) for k in ("omegaPtr", "rowPtr", "colI"))
+    m, n, k = int(enc["m"]), int(enc["n"]), omega.size
+    if np.unique(omega).size != k:
+        return ("omega", 0, "duplicate alphabet values")
+    segs = op.size - 1
+    if rp.size != m + 1:
+        return ("rowPtr", 0, f"expected {m + 1} entries")
+    for name, arr, last in (("omegaPtr", op, col.size), ("rowPtr", rp, segs)):
+        v = _first_monotone_violation(name, arr, 0, last)
+        if v:
+            return v
+    segs_per_row = np.diff(rp.astype(np.int64))
+    seg_row = np.repeat(np.arange(m), segs_per_row)
+    seg_len = np.diff(op.astype(np.int64))
+    v = _first_column_violation(col, op, n, np.repeat(seg_row, seg_len))
+    if v:
+        return v
+    if enc["kind"] == "cer":
+        over = np.flatnonzero(segs_per_row > k - 1)
+        if over.size:
+            r = int(over[0])
+            return ("rowPtr", r + 1,
+                    f"row holds {int(segs_per_row[r])} segments, alphabet has {k - 1} non-background elements")
+        if segs:
+            last_seg = (rp.astype(np.int64)[1:] - 1)[segs_per_row > 0]
+            hollow = np.flatnonzero(seg_len[last_seg] == 0)
+            if hollow.size:
+                return ("omegaPtr", int(last_seg[hollow[0]]) + 1, "trailing empty segment")
+        return None
+    oi = np.asarray(enc["omegaI"])
+    mode = int(enc["mode_index"])
+    if np.any(np.diff(omega) <= 0):
+        return ("omega", 0, "alphabet must be value-ascending")
+    if oi.size != segs:
+        return ("omegaI", 0, f"expected {segs} entries, found {oi.size}")
+    if not 0 <= mode < k:
+        return ("omega", mode, "mode_index out of range")
+    o = oi.astype(np.int64)
+    for bad, reason in ((o >= k, "element index out of range"),
+                        (o == mode, "segment references the background element")):
+        hit = np.flatnonzero(bad)
+        if hit.size:
+            return ("omegaI", int(hit[0]), reason)
+    hollow = np.flatnonzero(seg_len == 0)
+    if hollow.size:
+        return ("omegaPtr", int(hollow[0]) + 1, "empty segment")
+    dup = _first_duplicate(seg_row * k + o)
+    if dup is not None:
+        return ("omegaI", dup, "row references an element twice")
+    return None
+
+
+def decode(enc: dict) -> np.ndarray:
+    """Dense float64 reconstruction (formats.py:395-424); the encoding must be valid."""
+    omega = np.asarray(enc["omega"], dtype=np.float64)
+    op, rp = np.asarray(enc["omegaPtr"]).astype(np.int64), np.asarray(enc["rowPtr"]).astype(np.int64)
+    m, n = int(enc["m"]), int(enc["n"])
+    seg_row = np.repeat(np.arange(m), np.diff(rp))
+    seg_len = np.diff(op)
+    if enc["kind"] == "cer":
+        bg = omega[0]
+        seg_val = omega[np.arange(seg_len.size) - rp[:-1][seg_row] + 1]
+    else:
+        bg = omega[int(enc["mode_index"])]
+        seg_val = omega[np.asarray(enc["omegaI"]).astype(np.int64)]
+    out = np.full((m, n), bg)
+    out[np.repeat(seg_row, seg_len), np.asarray(enc["colI"]).astype(np.int64)] = np.repeat(seg_val, seg_len)
+    return out

@@ -72,3 +72,33 @@ def has_gpu() -> bool:
         return torch.cuda.is_available()
     except Exception:  # pragma: no cover
         return False
+
+
+def validate_case_arrays(bases, case) -> dict:
+    """The (possibly corrupted) encoding of one tests/golden/validate_cases.json case, as an oracle dict."""
+    base = bases[case["base"]]
+    enc = {k: (list(v) if isinstance(v, list) else v) for k, v in base.items() if k != "widths"}
+    if "set" in case:
+        name, pos, value = case["set"]
+        enc[name][pos] = value
+    if "drop" in case:
+        enc[case["drop"]] = enc[case["drop"]][:-1]
+    if case.get("omega_swap") and len(enc["omega"]) > 2:
+        enc["omega"][1], enc["omega"][2] = enc["omega"][2], enc["omega"][1]
+    if case.get("omega_dup") and len(enc["omega"]) > 1:
+        enc["omega"][-1] = enc["omega"][0]
+    if "mode" in case:
+        enc["mode_index"] = case["mode"]
+    out = {"kind": enc["kind"], "m": enc["m"], "n": enc["n"], "omega": np.asarray(enc["omega"], dtype=np.float64)}
+    for k in ("colI", "omegaPtr", "rowPtr", "omegaI"):
+        if k in enc:
+            out[k] = np.asarray(enc[k], dtype=np.dtype(f"uint{base['widths'][k]}"))
+    if "mode_index" in enc:
+        out["mode_index"] = enc["mode_index"]
+    return out
+
+
+@pytest.fixture(scope="session")
+def validate_cases():
+    with open(os.path.join(GOLDEN, "validate_cases.json")) as f:
+        return json.load(f)

@@ -146,3 +146,22 @@ def test_dimension_mismatch_message():
         numpy_port.dot(enc, np.ones(5))
     with pytest.raises(ValueError, match="mismatch"):
         c_oracle.dot(enc, np.ones(5))
+
+
+def test_oracle_validate_decode_vs_reference_fixtures(validate_cases):
+    """numpy_port.validate / decode against lemt.formats.validate / decode outcomes
+    (tests/golden/make_validate_golden.py): same (array, offset, reason) for every corrupted encoding,
+    same dense matrix (sha256) for every accepted one."""
+    import hashlib
+
+    from conftest import validate_case_arrays
+
+    bases = validate_cases["bases"]
+    for case in validate_cases["cases"]:
+        enc = validate_case_arrays(bases, case)
+        got = numpy_port.validate(enc)
+        want = tuple(case["error"]) if case["error"] else None
+        assert got == want, (case, got)
+        if want is None:
+            dense = numpy_port.decode(enc)
+            assert hashlib.sha256(np.ascontiguousarray(dense).tobytes()).hexdigest() == case["decode_sha256"], case
