@@ -55,7 +55,8 @@ typedef enum {
   CERDOT_E_INDEX = 3,
   CERDOT_E_CUDA = 4,
   CERDOT_E_UNSUPPORTED = 5,
-  CERDOT_E_WORKSPACE = 6 /* workspace too small: info->workspace_bytes holds the need */
+  CERDOT_E_WORKSPACE = 6, /* workspace too small: info->workspace_bytes holds the need */
+  CERDOT_E_FORMAT = 7     /* cerdot_validate found a structural violation (-> FormatError) */
 } cerdot_status;
 
 typedef enum { CERDOT_CER = 0, CERDOT_CSER = 1 } cerdot_kind;
@@ -172,6 +173,47 @@ int cerdot_dot_host(const cerdot_matrix *a, const float *x_host, int64_t ldx, in
 /* Derived index for cerdot_matrix.row_entry: out[r] = omega_ptr[row_ptr[r]] for r in [0, m], u32
  * (device, m+1).  CERDOT_E_VALUE when nnz does not fit 32 bits.  Stream-ordered. */
 int cerdot_row_entries(const cerdot_matrix *a, uint32_t *out, void *stream);
+
+/* Structural validation of an (untrusted) encoding on the device -- lemt.formats.validate
+ * (formats.py:298-392) for the index arrays.  The checks run in the reference's order; the first
+ * violation is written to *err (check id, offset into the named array, and the value its message
+ * quotes) and CERDOT_E_FORMAT returned; CERDOT_OK when every check passes.  The alphabet checks
+ * (duplicate / unsorted omega, mode_index range) and array-length checks are the caller's: the
+ * matrix struct carries lengths, not arrays of other lengths.  Synchronises `stream`. */
+typedef enum {
+  CERDOT_CHECK_NONE = 0,
+  CERDOT_CHECK_PTR_START,         /* omegaPtr[0] != 0                 ("must start at 0, found v") */
+  CERDOT_CHECK_PTR_ORDER,         /* omegaPtr decreasing at offset     ("must be non-decreasing") */
+  CERDOT_CHECK_PTR_END,           /* omegaPtr[segs] != nnz             ("must end at nnz, found v") */
+  CERDOT_CHECK_ROW_START,         /* rowPtr[0] != 0 */
+  CERDOT_CHECK_ROW_ORDER,         /* rowPtr decreasing */
+  CERDOT_CHECK_ROW_END,           /* rowPtr[m] != segments */
+  CERDOT_CHECK_COL_RANGE,         /* colI[offset] = v >= n */
+  CERDOT_CHECK_COL_ORDER,         /* colI not strictly ascending inside a segment */
+  CERDOT_CHECK_COL_DUPLICATE,     /* a column twice in one row (offset = second occurrence) */
+  CERDOT_CHECK_CER_ROW_SEGMENTS,  /* rowPtr[offset]: the row holds v > k-1 segments */
+  CERDOT_CHECK_CER_TRAILING_EMPTY,/* omegaPtr[offset]: a row ends with an empty segment */
+  CERDOT_CHECK_OI_RANGE,          /* omegaI[offset] >= k */
+  CERDOT_CHECK_OI_BACKGROUND,     /* omegaI[offset] == mode_index */
+  CERDOT_CHECK_EMPTY_SEGMENT,     /* omegaPtr[offset]: CSER segment without entries */
+  CERDOT_CHECK_OI_DUPLICATE,      /* an element twice in one row (offset = second occurrence) */
+  CERDOT_CHECK_COUNT
+} cerdot_check;
+
+typedef struct {
+  int32_t check;   /* cerdot_check */
+  int64_t offset;  /* position in the array the check names */
+  int64_t value;   /* the value the reference's message quotes (found start/end, column, segments) */
+} cerdot_format_error;
+
+size_t cerdot_validate_workspace_bytes(const cerdot_matrix *a);
+int cerdot_validate(const cerdot_matrix *a, cerdot_format_error *err, void *workspace, size_t workspace_bytes,
+                    void *stream);
+
+/* Dense reconstruction (lemt.formats.decode, formats.py:395-424) of a VALID encoding: out (device,
+ * m x n float64, row stride ldo) = background, then every segment's element at its columns.
+ * Stream-ordered. */
+int cerdot_decode(const cerdot_matrix *a, double *out, int64_t ldo, void *stream);
 
 /* Row-shard planner (host).  row_ptr / omega_ptr are HOST arrays of the
  * given widths.  Writes parts+1 row bounds (bounds[0]=0, bounds[parts]=m)

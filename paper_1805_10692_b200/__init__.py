@@ -13,18 +13,20 @@ from .formats import (
     CserMatrix,
     FormatError,
     array_bytes,
+    decode,
     encode_cer,
     encode_cser,
     entry_count,
     index_bitwidth,
     storage_bits,
+    validate,
 )
 from .kernels import OpTrace, dot, dot_cer, dot_cser, dot_device, row_trace, trace_cer, trace_cser, trace_of
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "DenseMatrix", "Vector", "CerMatrix", "CserMatrix", "FormatError", "array_bytes", "encode_cer",
+    "DenseMatrix", "Vector", "CerMatrix", "CserMatrix", "FormatError", "array_bytes", "decode", "validate", "encode_cer",
     "encode_cser", "entry_count", "index_bitwidth", "storage_bits", "OpTrace", "dot", "dot_cer", "dot_cser",
     "dot_device", "row_trace", "trace_cer", "trace_cser", "trace_of",
 ]

@@ -16,10 +16,14 @@ ROOT = os.path.dirname(PKG)
 LIB_PATH = os.environ.get("CERDOT_LIB") or os.path.join(PKG, "_lib", "libcerdot.so")
 HEADER = os.path.join(ROOT, "include", "cerdot.h")
 
-OK, E_VALUE, E_TYPE, E_INDEX, E_CUDA, E_UNSUPPORTED, E_WORKSPACE = range(7)
+OK, E_VALUE, E_TYPE, E_INDEX, E_CUDA, E_UNSUPPORTED, E_WORKSPACE, E_FORMAT = range(8)
 CER, CSER = 0, 1
 F32, F64 = 0, 1
 FAST_K = 2048
+
+
+class CerdotFormatError(ctypes.Structure):  # cerdot_format_error
+    _fields_ = [("check", ctypes.c_int32), ("offset", ctypes.c_int64), ("value", ctypes.c_int64)]
 
 
 class CerdotMatrix(ctypes.Structure):
@@ -80,6 +84,10 @@ _SIGNATURES = {
                                           _P, _I32, _P, _I32, _P]),
     "cerdot_dot_workspace_bytes": (_SZ, [ctypes.POINTER(CerdotMatrix), _I64]),
     "cerdot_dot": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _SZ, _P]),
+    "cerdot_validate_workspace_bytes": (_SZ, [ctypes.POINTER(CerdotMatrix)]),
+    "cerdot_validate": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), ctypes.POINTER(CerdotFormatError), _P, _SZ,
+                                       _P]),
+    "cerdot_decode": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _P]),
     "cerdot_dot_peers": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _I32, _I64, _P,
                                         _SZ, _P]),
     "cerdot_dot_cer": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _SZ, _P]),

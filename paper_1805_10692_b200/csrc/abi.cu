@@ -126,6 +126,25 @@ size_t cerdot_dot_workspace_bytes(const cerdot_matrix *a, int64_t batch) {
   return sizeof(double) * static_cast<size_t>(batch) * (batch > 1 ? 17 : 1);
 }
 
+size_t cerdot_validate_workspace_bytes(const cerdot_matrix *a) {
+  return a ? cerdot::validate_workspace_bytes(a) : 0;
+}
+
+int cerdot_validate(const cerdot_matrix *a, cerdot_format_error *err, void *workspace, size_t workspace_bytes,
+                    void *stream) {
+  if (a == nullptr || err == nullptr) return fail(CERDOT_E_VALUE, "validate: null matrix or error record");
+  if (a->m < 0 || a->n < 0 || a->k < 0 || a->nnz < 0 || a->segments < 0)
+    return fail(CERDOT_E_VALUE, "validate: negative sizes");
+  int rc = cerdot::validate(a, err, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+  if (rc) return rc;
+  return err->check == CERDOT_CHECK_NONE ? CERDOT_OK : fail(CERDOT_E_FORMAT, "structural violation (see the error record)");
+}
+
+int cerdot_decode(const cerdot_matrix *a, double *out, int64_t ldo, void *stream) {
+  if (a == nullptr || out == nullptr || ldo < a->n) return fail(CERDOT_E_VALUE, "decode: bad output");
+  return cerdot::decode(a, out, ldo, static_cast<cudaStream_t>(stream));
+}
+
 int cerdot_dot_peers(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,
                      float *const *peers, int32_t npeers, int64_t peer_offset, void *workspace,
                      size_t workspace_bytes, void *stream) {

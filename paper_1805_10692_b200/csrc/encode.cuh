@@ -26,4 +26,9 @@ int dot(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, floa
         size_t workspace_bytes, cudaStream_t st, float *const *peers = nullptr, int npeers = 0,
         int64_t peer_offset = 0);
 
+size_t validate_workspace_bytes(const cerdot_matrix *a);
+int validate(const cerdot_matrix *a, cerdot_format_error *err, void *workspace, size_t workspace_bytes,
+             cudaStream_t st);
+int decode(const cerdot_matrix *a, double *out, int64_t ldo, cudaStream_t st);
+
 }  // namespace cerdot

@@ -155,8 +155,11 @@ class DeviceEncoding:
         return sum(self.nbytes(nm) for nm in self.offsets if nm != "rowEntry")
 
     @classmethod
-    def from_host(cls, kind: int, m: int, n: int, mode_index: int, arrays: dict, device=None) -> "DeviceEncoding":
-        """Upload host arrays (any unsigned-representable ints) narrowed to 8/16/32 bits."""
+    def from_host(cls, kind: int, m: int, n: int, mode_index: int, arrays: dict, device=None,
+                  derive: bool = True) -> "DeviceEncoding":
+        """Upload host arrays (any unsigned-representable ints) narrowed to 8/16/32 bits.  ``derive=False``
+        skips the row statistics and the rowEntry index, which index through the pointers: the upload
+        of an untrusted encoding for validation."""
         torch = torch_mod()
         dev = require_cuda(device)
         omega = np.ascontiguousarray(arrays["omega"], dtype=np.float64)
@@ -183,7 +186,12 @@ class DeviceEncoding:
         for name, a in host.items():
             buf[offsets[name]:offsets[name] + a.nbytes] = a.view(np.uint8)
         arena = staging.to(dev, non_blocking=True)
-        bg = float(omega[mode_index] if kind == _native.CSER else omega[0]) if k else 0.0
+        bi = mode_index if kind == _native.CSER else 0
+        bg = float(omega[bi]) if 0 <= bi < k else 0.0  # (an out-of-range mode_index is validate's to report)
+        if not derive:
+            enc = cls(kind, m, n, k, nnz, segs, mode_index, bg, bits, arena, offsets, 0, 0)
+            torch.cuda.current_stream(dev).synchronize()  # the pinned staging buffer goes out of scope
+            return enc
         rp = host["rowPtr"].astype(np.int64)
         optr = host["omegaPtr"].astype(np.int64)
         seg_rows = np.diff(rp) if m else np.zeros(0, dtype=np.int64)

@@ -14,6 +14,8 @@ uploaded on its first dot product.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from . import _native
@@ -206,6 +208,104 @@ class CserMatrix(_Encoded):
 
 
 EncodedMatrix = CerMatrix | CserMatrix
+
+
+# --------------------------------------------------------------------------- validate / decode
+
+# cerdot_check id -> (array, reason template); {v} is the record's value, {last}/{n}/{k1} the sizes
+_CHECKS = {
+    1: ("omegaPtr", "must start at 0, found {v}"),
+    2: ("omegaPtr", "must be non-decreasing"),
+    3: ("omegaPtr", "must end at {nnz}, found {v}"),
+    4: ("rowPtr", "must start at 0, found {v}"),
+    5: ("rowPtr", "must be non-decreasing"),
+    6: ("rowPtr", "must end at {segs}, found {v}"),
+    7: ("colI", "column {v} out of range for n={n}"),
+    8: ("colI", "must be strictly ascending within a segment"),
+    9: ("colI", "duplicate column within a row"),
+    10: ("rowPtr", "row holds {v} segments, alphabet has {k1} non-background elements"),
+    11: ("omegaPtr", "trailing empty segment"),
+    12: ("omegaI", "element index out of range"),
+    13: ("omegaI", "segment references the background element"),
+    14: ("omegaPtr", "empty segment"),
+    15: ("omegaI", "row references an element twice"),
+}
+_LAST_COLUMN_CHECK = 9
+
+
+def _device_checks(x, device=None):
+    """Run cerdot_validate on the encoding (a validation-only upload of host-constructed arrays: no
+    derived indices).  Returns the error record's (check, offset, value)."""
+    torch = torch_mod()
+    dev = x._dev
+    if dev is None:
+        arrays = {"omega": x.omega, "colI": x.col_index, "omegaPtr": x.omega_ptr, "rowPtr": x.row_ptr}
+        if x._kind == _native.CSER:  # length errors are reported later, in the reference's order
+            segs = len(x.omega_ptr) - 1
+            oi = np.asarray(x.omega_index)
+            arrays["omegaI"] = oi[:segs] if oi.size >= segs else np.concatenate(
+                [oi, np.zeros(segs - oi.size, dtype=oi.dtype)])
+        dev = DeviceEncoding.from_host(x._kind, x.m, x.n, x.mode_index, arrays, device, derive=False)
+    L = _native.lib()
+    st = dev.struct()
+    nbytes = L.cerdot_validate_workspace_bytes(st)
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev.device)
+    rec = _native.CerdotFormatError()
+    with torch.cuda.device(dev.device):
+        rc = L.cerdot_validate(st, ctypes.byref(rec), ws.data_ptr(), nbytes, stream_ptr(dev.device))
+    if rc not in (_native.OK, _native.E_FORMAT):
+        _native.check(rc)
+    return rec.check, rec.offset, rec.value
+
+
+def validate(x) -> None:
+    """Raise FormatError on any structural inconsistency (formats.py:331-392), checked on the device.
+
+    The alphabet and length checks run here (host, tiny arrays); the index arrays are checked by
+    ``cerdot_validate`` in the reference's order, so the same first violation is reported.
+    """
+    if not isinstance(x, (CerMatrix, CserMatrix)):
+        raise TypeError(f"not an encoded matrix: {type(x)!r}")
+    omega = np.asarray(x.omega, dtype=np.float64)
+    k = omega.size
+    if np.unique(omega).size != k:
+        raise FormatError("omega", 0, "duplicate alphabet values")
+    if len(x.row_ptr) != x.m + 1:
+        raise FormatError("rowPtr", 0, f"expected {x.m + 1} entries")
+    if len(x.omega_ptr) == 0:
+        raise FormatError("omegaPtr", 0, "array is empty")
+    check, offset, value = _device_checks(x)
+    sizes = {"nnz": x.nnz, "segs": len(x.omega_ptr) - 1, "n": x.n, "k1": k - 1}
+
+    def fail(c):
+        array, reason = _CHECKS[c]
+        raise FormatError(array, int(offset), reason.format(v=int(value), **sizes))
+
+    if check and (check <= _LAST_COLUMN_CHECK or isinstance(x, CerMatrix)):
+        fail(check)
+    if isinstance(x, CserMatrix):
+        if np.any(np.diff(omega) <= 0):
+            raise FormatError("omega", 0, "alphabet must be value-ascending")
+        segs = len(x.omega_ptr) - 1
+        if len(x.omega_index) != segs:
+            raise FormatError("omegaI", 0, f"expected {segs} entries, found {len(x.omega_index)}")
+        if not 0 <= x.mode_index < k:
+            raise FormatError("omega", x.mode_index, "mode_index out of range")
+        if check:
+            fail(check)
+
+
+def decode(x):
+    """Exact dense reconstruction (formats.py:395-424) on the device; validates first."""
+    if isinstance(x, DenseMatrix):
+        return x
+    validate(x)
+    torch = torch_mod()
+    dev = x.device_encoding()
+    out = torch.empty((x.m, x.n), dtype=torch.float64, device=dev.device)
+    with torch.cuda.device(dev.device):
+        _native.check(_native.lib().cerdot_decode(dev.struct(), out.data_ptr(), max(x.n, 1), stream_ptr(dev.device)))
+    return DenseMatrix(out.cpu().numpy(), element_bits=x.element_bits)
 
 
 # --------------------------------------------------------------------------- conversion

@@ -474,3 +474,40 @@ def test_peer_row_sharded_dot_single_rank():
         assert torch.equal(y, cd.dot_device(enc, x))
     finally:
         dist.destroy_process_group()
+
+
+def test_device_validate_and_decode_match_reference(validate_cases):
+    """cd.validate (cerdot_validate on the device) raises the reference's FormatError -- same array,
+    offset and reason -- for all 1395 corrupted encodings of tests/golden/validate_cases.json, and
+    cd.decode reproduces the reference's dense matrix (sha256) for every accepted one."""
+    import hashlib
+
+    from conftest import validate_case_arrays
+
+    bases = validate_cases["bases"]
+    for case in validate_cases["cases"]:
+        e = validate_case_arrays(bases, case)
+        if e["kind"] == "cer":
+            enc = cd.CerMatrix(e["omega"], e["colI"], e["omegaPtr"], e["rowPtr"], e["m"], e["n"])
+        else:
+            enc = cd.CserMatrix(e["omega"], e["colI"], e["omegaI"], e["omegaPtr"], e["rowPtr"], e["m"], e["n"],
+                                mode_index=e["mode_index"])
+        if case["error"]:
+            with pytest.raises(cd.FormatError) as err:
+                cd.validate(enc)
+            got = [err.value.array, err.value.offset, err.value.reason]
+            assert got == case["error"], (case, got)
+        else:
+            cd.validate(enc)
+            dense = cd.decode(enc).values
+            assert hashlib.sha256(np.ascontiguousarray(dense).tobytes()).hexdigest() == case["decode_sha256"], case
+
+
+@pytest.mark.parametrize("name", ["oracle", "alexnet-fc6", "resnet-conv"])
+def test_device_decode_round_trip_configs(name):
+    """Encoder output validates and decodes back to W exactly (the reference's TestRoundTrip), device-resident."""
+    w, _ = synth.make_layer(name)
+    for encode in (cd.encode_cer, cd.encode_cser):
+        enc = encode(torch.from_numpy(w).cuda())
+        cd.validate(enc)
+        assert np.array_equal(cd.decode(enc).values, w.astype(np.float64)), (name, encode.__name__)
