@@ -511,3 +511,42 @@ def test_device_decode_round_trip_configs(name):
         enc = encode(torch.from_numpy(w).cuda())
         cd.validate(enc)
         assert np.array_equal(cd.decode(enc).values, w.astype(np.float64)), (name, encode.__name__)
+
+
+def test_corruption_fuzz_every_single_entry():
+    """The reference's TestCorruptionFuzz (tests/test_formats.py:214-235) on the device: EVERY
+    (position, value) corruption of M's pointer and omegaI arrays; >= 99% rejected, and each outcome
+    identical to the pinned oracle's."""
+    from oracle import numpy_port
+
+    w = np.array([[0, 3, 0, 2, 4, 0, 0, 2, 3, 4, 0, 4], [4, 4, 0, 0, 0, 4, 0, 0, 4, 4, 0, 4],
+                  [4, 0, 3, 4, 0, 0, 0, 4, 0, 2, 0, 0], [0, 0, 0, 4, 4, 4, 0, 3, 4, 4, 0, 0],
+                  [0, 4, 4, 0, 0, 4, 0, 4, 0, 0, 0, 0]], dtype=float)
+    for kind in ("cer", "cser"):
+        base = (numpy_port.encode_cer if kind == "cer" else numpy_port.encode_cser)(w)
+        names = ["omegaPtr", "rowPtr"] + (["omegaI"] if kind == "cser" else [])
+        for name in names:
+            arr = np.asarray(base[name])
+            total = accepted = 0
+            for pos in range(arr.size):
+                for value in range(1 << (arr.dtype.itemsize * 8)):
+                    if value == arr[pos]:
+                        continue
+                    e = dict(base)
+                    e[name] = arr.copy()
+                    e[name][pos] = value
+                    if kind == "cer":
+                        enc = cd.CerMatrix(e["omega"], e["colI"], e["omegaPtr"], e["rowPtr"], e["m"], e["n"])
+                    else:
+                        enc = cd.CserMatrix(e["omega"], e["colI"], e["omegaI"], e["omegaPtr"], e["rowPtr"], e["m"],
+                                            e["n"], mode_index=e["mode_index"])
+                    want = numpy_port.validate(e)
+                    total += 1
+                    try:
+                        cd.validate(enc)
+                        got = None
+                    except cd.FormatError as err:
+                        got = (err.array, err.offset, err.reason)
+                    assert got == want, (kind, name, pos, value, got, want)
+                    accepted += got is None
+            assert 1.0 - accepted / total >= 0.99, (kind, name, accepted, total)
