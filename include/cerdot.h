@@ -215,6 +215,14 @@ int cerdot_validate(const cerdot_matrix *a, cerdot_format_error *err, void *work
  * Stream-ordered. */
 int cerdot_decode(const cerdot_matrix *a, double *out, int64_t ldo, void *stream);
 
+/* LEMX container loader (lemt io.py:177-278), device half: `payload` (device) holds the container's
+ * array payload as read from the file (everything after the fixed header).  omega (k elements of
+ * element_bits: f64 / f32 / f16 / i8, at payload offset omega_offset) is widened to f64 into `omega`;
+ * each of `count` (<= 4) index arrays is copied byte for byte: spans (HOST) holds count triples
+ * (payload offset, arena offset, bytes).  The host parses and checks the header.  Stream-ordered. */
+int cerdot_lemx_unpack(const void *payload, int32_t element_bits, int64_t k, int64_t omega_offset, double *omega,
+                       const int64_t *spans, int32_t count, void *arena, void *stream);
+
 /* Row-shard planner (host).  row_ptr / omega_ptr are HOST arrays of the
  * given widths.  Writes parts+1 row bounds (bounds[0]=0, bounds[parts]=m)
  * splitting rows into contiguous blocks of near-equal encoded bytes

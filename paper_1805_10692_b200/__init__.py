@@ -21,6 +21,7 @@ from .formats import (
     storage_bits,
     validate,
 )
+from .io import IoFormatError, read_matrix, write_matrix
 from .kernels import OpTrace, dot, dot_cer, dot_cser, dot_device, row_trace, trace_cer, trace_cser, trace_of
 
 __version__ = "0.1.0"
@@ -28,5 +29,6 @@ __version__ = "0.1.0"
 __all__ = [
     "DenseMatrix", "Vector", "CerMatrix", "CserMatrix", "FormatError", "array_bytes", "decode", "validate", "encode_cer",
     "encode_cser", "entry_count", "index_bitwidth", "storage_bits", "OpTrace", "dot", "dot_cer", "dot_cser",
-    "dot_device", "row_trace", "trace_cer", "trace_cser", "trace_of",
+    "dot_device", "row_trace", "trace_cer", "trace_cser", "trace_of", "IoFormatError", "read_matrix",
+    "write_matrix",
 ]

@@ -145,6 +145,14 @@ int cerdot_decode(const cerdot_matrix *a, double *out, int64_t ldo, void *stream
   return cerdot::decode(a, out, ldo, static_cast<cudaStream_t>(stream));
 }
 
+int cerdot_lemx_unpack(const void *payload, int32_t element_bits, int64_t k, int64_t omega_offset, double *omega,
+                       const int64_t *spans, int32_t count, void *arena, void *stream) {
+  if (payload == nullptr || omega == nullptr || (count > 0 && (spans == nullptr || arena == nullptr)))
+    return fail(CERDOT_E_VALUE, "lemx_unpack: null buffer");
+  return cerdot::lemx_unpack(payload, element_bits, k, omega_offset, omega, spans, count, arena,
+                             static_cast<cudaStream_t>(stream));
+}
+
 int cerdot_dot_peers(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,
                      float *const *peers, int32_t npeers, int64_t peer_offset, void *workspace,
                      size_t workspace_bytes, void *stream) {
