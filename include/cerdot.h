@@ -215,6 +215,11 @@ int cerdot_validate(const cerdot_matrix *a, cerdot_format_error *err, void *work
  * Stream-ordered. */
 int cerdot_decode(const cerdot_matrix *a, double *out, int64_t ldo, void *stream);
 
+/* Inputs of the analytic OpTrace (lemt kernels.py:175-234) over all rows, counted on the device:
+ * counts (HOST, 5) = segments, non-empty segments, entries, rows holding segments, and the sum over
+ * rows of max(non-empty segments - 1, 0).  workspace: 64 device bytes.  Synchronises `stream`. */
+int cerdot_trace_counts(const cerdot_matrix *a, uint64_t *counts, void *workspace, void *stream);
+
 /* LEMX container loader (lemt io.py:177-278), device half: `payload` (device) holds the container's
  * array payload as read from the file (everything after the fixed header).  omega (k elements of
  * element_bits: f64 / f32 / f16 / i8, at payload offset omega_offset) is widened to f64 into `omega`;

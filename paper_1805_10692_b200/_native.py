@@ -88,6 +88,7 @@ _SIGNATURES = {
     "cerdot_validate": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), ctypes.POINTER(CerdotFormatError), _P, _SZ,
                                        _P]),
     "cerdot_decode": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _P]),
+    "cerdot_trace_counts": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _P, _P]),
     "cerdot_lemx_unpack": (ctypes.c_int, [_P, _I32, _I64, _I64, _P, _P, _I32, _P, _P]),
     "cerdot_dot_peers": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _I32, _I64, _P,
                                         _SZ, _P]),

@@ -145,6 +145,11 @@ int cerdot_decode(const cerdot_matrix *a, double *out, int64_t ldo, void *stream
   return cerdot::decode(a, out, ldo, static_cast<cudaStream_t>(stream));
 }
 
+int cerdot_trace_counts(const cerdot_matrix *a, uint64_t *counts, void *workspace, void *stream) {
+  if (a == nullptr || counts == nullptr || workspace == nullptr) return fail(CERDOT_E_VALUE, "trace_counts: null");
+  return cerdot::trace_counts(a, counts, workspace, static_cast<cudaStream_t>(stream));
+}
+
 int cerdot_lemx_unpack(const void *payload, int32_t element_bits, int64_t k, int64_t omega_offset, double *omega,
                        const int64_t *spans, int32_t count, void *arena, void *stream) {
   if (payload == nullptr || omega == nullptr || (count > 0 && (spans == nullptr || arena == nullptr)))

@@ -30,6 +30,7 @@ size_t validate_workspace_bytes(const cerdot_matrix *a);
 int validate(const cerdot_matrix *a, cerdot_format_error *err, void *workspace, size_t workspace_bytes,
              cudaStream_t st);
 int decode(const cerdot_matrix *a, double *out, int64_t ldo, cudaStream_t st);
+int trace_counts(const cerdot_matrix *a, uint64_t *counts, void *workspace, cudaStream_t st);
 int lemx_unpack(const void *payload, int element_bits, int64_t k, int64_t omega_src, double *omega,
                 const int64_t *spans, int count, void *arena, cudaStream_t st);
 

@@ -177,6 +177,34 @@ __global__ void k_decode_scatter(cerdot_matrix a, double *out, int64_t ldo) {
   }
 }
 
+// Trace counts (kernels.py:175-234 inputs) over all rows: segments, non-empty segments, entries,
+// rows with segments, sum over rows of max(non-empty - 1, 0).  Thread per row; integer atomics.
+__global__ void k_trace_counts(cerdot_matrix a, unsigned long long *out) {
+  unsigned long long c[5] = {0, 0, 0, 0, 0};
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < a.m;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t s0 = load_index(a.row_ptr, a.row_ptr_bits, r), s1 = load_index(a.row_ptr, a.row_ptr_bits, r + 1);
+    uint32_t ne = 0, prev = load_index(a.omega_ptr, a.omega_ptr_bits, s0);
+    const uint32_t first = prev;
+    for (uint32_t s = s0; s < s1; ++s) {
+      const uint32_t nxt = load_index(a.omega_ptr, a.omega_ptr_bits, s + 1);
+      ne += nxt > prev;
+      prev = nxt;
+    }
+    c[0] += s1 - s0;
+    c[1] += ne;
+    c[2] += prev - first;
+    c[3] += s1 > s0;
+    c[4] += ne > 0 ? ne - 1 : 0;
+  }
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    unsigned long long v = c[i];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out + i, v);
+  }
+}
+
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 int64_t dup_grid(int64_t m) { return std::max<int64_t>(1, std::min<int64_t>(m, int64_t(num_sms()) * 2)); }
@@ -285,6 +313,18 @@ int validate(const cerdot_matrix *a, cerdot_format_error *err, void *workspace, 
     if (c == CERDOT_CHECK_CER_TRAILING_EMPTY || c == CERDOT_CHECK_EMPTY_SEGMENT) off += 1;  // omegaPtr entry
     return report(c, off, value);
   }
+  return CERDOT_OK;
+}
+
+int trace_counts(const cerdot_matrix *a, uint64_t *counts, void *workspace, cudaStream_t st) {
+  unsigned long long *d = static_cast<unsigned long long *>(workspace);
+  CERDOT_CUDA_CHECK(cudaMemsetAsync(d, 0, 5 * sizeof(unsigned long long), st));
+  if (a->m > 0) {
+    k_trace_counts<<<grid_for(a->m), 256, 0, st>>>(*a, d);
+    CERDOT_LAUNCH_CHECK();
+  }
+  CERDOT_CUDA_CHECK(cudaMemcpyAsync(counts, d, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CERDOT_CUDA_CHECK(cudaStreamSynchronize(st));
   return CERDOT_OK;
 }
 

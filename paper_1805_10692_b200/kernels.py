@@ -16,6 +16,7 @@ encoding's row/segment structure; traces never change numeric results.
 
 from __future__ import annotations
 
+import ctypes
 import threading
 from dataclasses import dataclass, field
 
@@ -124,18 +125,34 @@ def _segment_shape(x, rows):
     return segs_per_row, nonempty, entries
 
 
+def _device_trace_counts(x):
+    """(rows, segments, non-empty, entries, rows with segments, sum max(non-empty - 1, 0)) counted on the
+    device (cerdot_trace_counts) for a device-resident encoding, without downloading its arrays."""
+    torch = torch_mod()
+    dev = x._dev
+    ws = torch.zeros(8, dtype=torch.int64, device=dev.device)
+    out = (ctypes.c_uint64 * 5)()
+    with torch.cuda.device(dev.device):
+        _native.check(_native.lib().cerdot_trace_counts(dev.struct(), out, ws.data_ptr(), stream_ptr(dev.device)))
+    return (x.m,) + tuple(int(v) for v in out)
+
+
 def _trace_segmented(x, input_bits, output_bits, rows, columns, with_omega_index) -> OpTrace:
     b_in, b_out = _resolve_bits(x, 32, input_bits, output_bits)
-    segs, nonempty, entries = _segment_shape(x, rows)
-    r = len(segs)
-    s, s_ne, z = int(segs.sum()), int(nonempty.sum()), int(entries.sum())
+    if rows is None and getattr(x, "_dev", None) is not None:
+        r, s, s_ne, z, rows_with_segs, extra_sums = _device_trace_counts(x)
+    else:
+        segs, nonempty, entries = _segment_shape(x, rows)
+        r = len(segs)
+        s, s_ne, z = int(segs.sum()), int(nonempty.sum()), int(entries.sum())
+        rows_with_segs, extra_sums = int((segs > 0).sum()), int(np.maximum(nonempty - 1, 0).sum())
     t = OpTrace()
     if x.background != 0.0:
         t.add("sum", b_in, TAG_NONE, max(x.n - 1, 0))
         t.add("mul", b_out, TAG_NONE, 1)
         t.add("sum", b_out, TAG_NONE, r + s_ne)
     t.add("read", x.row_ptr_bits, TAG_ROWPTR, 2 * r)
-    t.add("read", x.omega_ptr_bits, TAG_OMEGAPTR, s + int((segs > 0).sum()))
+    t.add("read", x.omega_ptr_bits, TAG_OMEGAPTR, s + rows_with_segs)
     if with_omega_index:
         t.add("read", x.omega_index_bits, TAG_OMEGAI, s)
     t.add("read", x.element_bits, TAG_OMEGA, s_ne)
@@ -143,7 +160,7 @@ def _trace_segmented(x, input_bits, output_bits, rows, columns, with_omega_index
     t.add("read", b_in, TAG_INPUT, z)
     t.add("sum", b_in, TAG_NONE, z - s_ne)
     t.add("mul", b_out, TAG_NONE, s_ne)
-    t.add("sum", b_out, TAG_NONE, int(np.maximum(nonempty - 1, 0).sum()))
+    t.add("sum", b_out, TAG_NONE, extra_sums)
     t.add("write", b_out, TAG_OUTPUT, r)
     t.add("other", 0, TAG_NONE, 3 * r + 4 * s + z + 1)
     return t.scaled(columns) if columns != 1 else t

@@ -550,3 +550,19 @@ def test_corruption_fuzz_every_single_entry():
                     assert got == want, (kind, name, pos, value, got, want)
                     accepted += got is None
             assert 1.0 - accepted / total >= 0.99, (kind, name, accepted, total)
+
+
+@pytest.mark.parametrize("name", ["oracle", "alexnet-fc6", "resnet-conv"])
+def test_device_trace_counts_match_host_trace(name):
+    """trace_of on a device-resident encoding (cerdot_trace_counts) == trace_of on the same arrays held
+    on the host (the reference's analytic trace, kernels.py:175-234), for 1 and 7 columns."""
+    w, _ = synth.make_layer(name)
+    for encode in (cd.encode_cer, cd.encode_cser):
+        enc = encode(torch.from_numpy(w).cuda())
+        if isinstance(enc, cd.CerMatrix):
+            host = cd.CerMatrix(enc.omega, enc.col_index, enc.omega_ptr, enc.row_ptr, enc.m, enc.n, enc.element_bits)
+        else:
+            host = cd.CserMatrix(enc.omega, enc.col_index, enc.omega_index, enc.omega_ptr, enc.row_ptr, enc.m, enc.n,
+                                 enc.element_bits, enc.mode_index)
+        for cols in (1, 7):
+            assert cd.trace_of(enc, columns=cols).counts == cd.trace_of(host, columns=cols).counts, (name, cols)
