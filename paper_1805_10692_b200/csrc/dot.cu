@@ -1720,9 +1720,15 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
     };
     // 8 X-row loads in flight for every V (measured: V = 4 at D = 4 runs 3 CTAs per SM instead of 2
     // but is slower on all of VGG fc6 B=128, ResNet conv B=1568 and 32768^2 B=256)
+    // V = 2 at 16 loads in flight (AlexNet fc6 B=64: 97 -> 80 us); V = 1 stays at 8 (16 is 9% slower at
+    // B=32).  CERDOT_MM_D forces 8 / 16 for V <= 2 (A/B only).
+    const char *fd = getenv("CERDOT_MM_D");
     if (V == 4) return go(k_matmat_flat<ColT, PtrT, CSER, 4, 8>);
-    if (V == 2) return go(k_matmat_flat<ColT, PtrT, CSER, 2, 8>);
-    return go(k_matmat_flat<ColT, PtrT, CSER, 1, 8>);
+    if (V == 2)
+      return (fd ? atoi(fd) : 16) == 16 ? go(k_matmat_flat<ColT, PtrT, CSER, 2, 16>)
+                                        : go(k_matmat_flat<ColT, PtrT, CSER, 2, 8>);
+    return (fd ? atoi(fd) : 8) == 16 ? go(k_matmat_flat<ColT, PtrT, CSER, 1, 16>)
+                                     : go(k_matmat_flat<ColT, PtrT, CSER, 1, 8>);
   }
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(units, 8),
                                                                            int64_t(num_sms()) * 8)));
