@@ -158,6 +158,9 @@ __global__ void __launch_bounds__(256) k_value_hist(const T *__restrict__ w, int
   unsigned int saw_pos0 = 0, saw_neg0 = 0;
   for (int64_t base = warp_id * 32; base < nvec; base += nwarps * 32) {
     const int64_t vi = base + lane;
+    // the grid-stride loop holds one 16 B load per lane: bring the lines of two steps ahead into L2
+    if (V > 1 && contig && (vi + 2 * nwarps * 32) * V + V <= total)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(w + (vi + 2 * nwarps * 32) * V));
     double vals[V];
     bool valid[V];
     if (V > 1 && vi * V + V <= total) {
@@ -340,11 +343,47 @@ __global__ void __launch_bounds__(kRowThreads) k_row_count(const T *__restrict__
   }
   RankT *ranks = static_cast<RankT *>(ws.ranks);
   const int lane = threadIdx.x & 31;
+  // vector path: VC consecutive columns per thread (one 16 B load), two loads in flight, the ranks
+  // stored packed, the histogram by predicated shared atomics (background rank 0 is not counted)
+  constexpr int VC = sizeof(T) == 4 ? 4 : 2;
+  const bool vec = (n % VC == 0) && (ldw % VC == 0) && (reinterpret_cast<uintptr_t>(w) % 16 == 0);
+  auto rank_of = [&](double v) -> unsigned int {
+    const unsigned long long kk = value_key(v);
+    uint32_t h = hash_key(kk) & (rcap - 1);
+    while (rkey[h] != kk) h = (h + 1) & (rcap - 1);
+    return rrank[h];
+  };
   for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
     for (unsigned int q = threadIdx.x; q < k; q += blockDim.x) hist[q] = 0;
     __syncthreads();
     const T *wr = w + row * ldw;
     RankT *rr = ranks + row * n;
+    if (vec) {
+#pragma unroll 2
+      for (int64_t c = static_cast<int64_t>(threadIdx.x) * VC; c < n; c += static_cast<int64_t>(blockDim.x) * VC) {
+        double v[VC];
+        VecLoad<T, VC>::load(wr + c, v);
+        unsigned int rk[VC];
+#pragma unroll
+        for (int j = 0; j < VC; ++j) {
+          rk[j] = rank_of(v[j]);
+          if (rk[j] != 0) atomicAdd(&hist[rk[j]], 1u);
+        }
+        if (sizeof(RankT) == 1) {
+          uint32_t pk = 0;
+#pragma unroll
+          for (int j = 0; j < VC; ++j) pk |= (rk[j] & 0xffu) << (8 * j);
+          if (VC == 4) *reinterpret_cast<uint32_t *>(rr + c) = pk;
+          else *reinterpret_cast<uint16_t *>(rr + c) = static_cast<uint16_t>(pk);
+        } else {
+          uint64_t pk = 0;
+#pragma unroll
+          for (int j = 0; j < VC; ++j) pk |= static_cast<uint64_t>(rk[j] & 0xffffu) << (16 * j);
+          if (VC == 4) *reinterpret_cast<uint64_t *>(rr + c) = pk;
+          else *reinterpret_cast<uint32_t *>(rr + c) = static_cast<uint32_t>(pk);
+        }
+      }
+    } else
     for (int64_t c0 = threadIdx.x - lane; c0 < n; c0 += blockDim.x) {
       const int64_t c = c0 + lane;
       unsigned int rk = 0;
@@ -468,11 +507,24 @@ __global__ void __launch_bounds__(kRowThreads) k_row_fill(int64_t m, int64_t n, 
     __syncthreads();
     const RankT *rr = ranks + row * n;
     const int64_t c_begin = wid * slab, c_end = min64(n, c_begin + slab);
-    for (int64_t c0 = c_begin; c0 < c_end; c0 += 32) {
-      const int64_t c = c0 + lane;
-      const unsigned int rk = c < c_end ? rr[c] : 0u;
-      const unsigned int peers = __match_any_sync(0xffffffffu, rk);
-      if (rk != 0 && lane == __ffs(peers) - 1) wc[wid * k + rk] += __popc(peers);
+    if (sizeof(RankT) == 1 && (slab & 3) == 0 && (n & 3) == 0) {
+      // count pass, 4 ranks per lane per load, predicated shared atomics (no match.any; the counts are
+      // order-free, only the scatter below needs lane order)
+      for (int64_t c = c_begin + 4 * lane; c < c_end; c += 128) {
+        const uint32_t pk = *reinterpret_cast<const uint32_t *>(rr + c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const unsigned int rk = (pk >> (8 * j)) & 0xffu;
+          if (rk != 0 && c + j < c_end) atomicAdd(&wc[wid * k + rk], 1u);
+        }
+      }
+    } else {
+      for (int64_t c0 = c_begin; c0 < c_end; c0 += 32) {
+        const int64_t c = c0 + lane;
+        const unsigned int rk = c < c_end ? rr[c] : 0u;
+        const unsigned int peers = __match_any_sync(0xffffffffu, rk);
+        if (rk != 0 && lane == __ffs(peers) - 1) wc[wid * k + rk] += __popc(peers);
+      }
     }
     __syncthreads();
     // per rank: total count and per-warp exclusive offsets

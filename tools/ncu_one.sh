@@ -4,7 +4,7 @@
 set -u
 tag=$1; kre=$2; shift 2
 mkdir -p gpurun_out
-timeout 300 ncu -f --set full --import-source on --clock-control none -k "regex:${kre}" --launch-skip 1 -c 1 \
+timeout 300 ncu -f --set full --import-source on --clock-control none -k "regex:${kre}" --launch-skip ${NCU_SKIP:-1} -c 1 \
   -o /tmp/ncu_$tag "$@" > gpurun_out/ncu_$tag.log 2>&1
 ncu -i /tmp/ncu_$tag.ncu-rep --page details > gpurun_out/$tag.details.txt 2>&1
 ncu -i /tmp/ncu_$tag.ncu-rep --page raw --csv > gpurun_out/$tag.raw.csv 2>&1
