@@ -134,7 +134,9 @@ def init_dist(use_cuda: bool):
             import torch
 
             torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if use_cuda else "gloo")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -451,6 +453,9 @@ def run_ours(args):
         try:  # y all-gather fused into the kernels' epilogue (NVLink peer stores), one barrier per step
             from paper_1805_10692_b200.shard import PeerRowShardedDot
 
+            if os.environ.get("CERDOT_EXCHANGE", "fused") == "nccl":
+                raise RuntimeError("CERDOT_EXCHANGE=nccl")
+
             shard_cer = [PeerRowShardedDot(c, rows, batch=1) for c in cers]
             shard_cser = [PeerRowShardedDot(c, rows, batch=1) for c in csers]
             exchange = "fused: cerdot_dot_peers epilogue stores to every rank's symmetric-memory buffer + one barrier"
@@ -559,7 +564,7 @@ def run_ours(args):
             },
             "gmacs": round(world * 2 * cfg.m * cfg.n / t_step / 1e9, 1),
             "roofline": {
-                "bound": "hbm", "kernel": "k_dot_vec (CER + CSER mat-vec)",
+                "bound": "hbm", "kernel": "k_matvec<u16,u32,CER|CSER,896 threads> (the CER and CSER mat-vec)",
                 "achieved": round(step_bytes / t_step / 1e9, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(step_bytes / t_step / 1e9 / peak, 4), "traffic": traffic.get("mean"),
                 "traffic_per_launch": traffic.get("per_launch"), "traffic_source": traffic.get("source"),
