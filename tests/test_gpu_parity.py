@@ -566,3 +566,25 @@ def test_device_trace_counts_match_host_trace(name):
                                  enc.element_bits, enc.mode_index)
         for cols in (1, 7):
             assert cd.trace_of(enc, columns=cols).counts == cd.trace_of(host, columns=cols).counts, (name, cols)
+
+
+def test_randomized_round_trip_and_dot():
+    """The reference's TestRoundTrip shape (random low-entropy matrices, tests/test_formats.py:142-150)
+    through the whole device path: encode (bit-exact vs the oracle), validate, decode == W, and the
+    mat-vec / mat-mat through every kernel path against the oracle (integer alphabets: bitwise)."""
+    rng = np.random.default_rng(1805)
+    for trial in range(60):
+        m, n, kk = int(rng.integers(1, 70)), int(rng.integers(1, 400)), int(rng.integers(1, 9))
+        elems = np.unique(rng.integers(-5, 6, size=kk)).astype(float)
+        wts = rng.random(elems.size) + 0.1
+        w = rng.choice(elems, size=(m, n), p=wts / wts.sum())
+        x = rng.integers(-3, 4, size=(n, 3)).astype(np.float64)
+        for kind, encode in (("cer", cd.encode_cer), ("cser", cd.encode_cser)):
+            enc = encode(cd.DenseMatrix(w))
+            ref = (numpy_port.encode_cer if kind == "cer" else numpy_port.encode_cser)(w)
+            assert np.array_equal(enc.col_index, ref["colI"]) and np.array_equal(enc.omega_ptr, ref["omegaPtr"])
+            assert np.array_equal(enc.row_ptr, ref["rowPtr"]) and np.array_equal(enc.omega, ref["omega"])
+            cd.validate(enc)
+            assert np.array_equal(cd.decode(enc).values, w), (trial, kind)
+            assert np.array_equal(cd.dot(enc, x), w @ x), (trial, kind)
+            assert np.array_equal(cd.dot(enc, x[:, 0]), w @ x[:, 0]), (trial, kind)
