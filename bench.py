@@ -418,10 +418,22 @@ def run_ours(args):
 
     cfg = synth.config(args.config)
     peak, peak_src = _peaks()
-    # ---- this rank's row block (weak scaling: seed + rank)
-    w, xs = synth.make_layer(cfg, seed=args.seed + rank)
-    x_host = xs[1] if 1 in xs else synth.make_inputs(cfg, np.random.default_rng(args.seed + 1), 1)
-    wt = torch.from_numpy(w).to(device)
+    strong = cfg.m * cfg.n > 10**9
+    if strong:
+        # config 5: ONE matrix row-sharded over the ranks (strong scaling); every rank draws only its
+        # row block on the device (synth.make_weights_device: a block is the same at any GPU count)
+        bounds = [cfg.m * r // world for r in range(world + 1)]
+        wt = synth.make_weights_device(cfg, args.seed, device, row0=bounds[rank], rows=bounds[rank + 1] - bounds[rank])
+        x_host = synth.make_inputs(cfg, np.random.default_rng(args.seed + 1), 1)
+        w = wt[: min(256, wt.shape[0])].cpu().numpy()  # CPU baseline sample (rows of the block)
+        rows = [bounds[r + 1] - bounds[r] for r in range(world)]
+    else:
+        # ---- this rank's row block (weak scaling: seed + rank)
+        w, xs = synth.make_layer(cfg, seed=args.seed + rank)
+        x_host = xs[1] if 1 in xs else synth.make_inputs(cfg, np.random.default_rng(args.seed + 1), 1)
+        wt = torch.from_numpy(w).to(device)
+        rows = [cfg.m] * world
+    m_local = int(wt.shape[0])
     cd.encode_cer(wt), cd.encode_cser(wt)  # warm the conversion kernels (first-launch setup)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -434,13 +446,15 @@ def run_ours(args):
     t_enc_cser = time.perf_counter() - t0
     step_bytes = alg_bytes(cer, 1) + alg_bytes(cser, 1)
     per_copy = cer.device_encoding().format_bytes + cser.device_encoding().format_bytes + 2 * x_host.nbytes
-    rotate = max(ROTATE_MIN, -(-2 * L2_BYTES // per_copy))
+    rotate = max(ROTATE_MIN if per_copy < L2_BYTES else 2, -(-2 * L2_BYTES // per_copy))
     cers = [_clone(cd, cer) for _ in range(rotate)]
     csers = [_clone(cd, cser) for _ in range(rotate)]
     xdev = [torch.from_numpy(x_host).to(device) for _ in range(rotate)]
-    ycer = [torch.empty(cfg.m, dtype=torch.float32, device=device) for _ in range(rotate)]
-    ycser = [torch.empty(cfg.m, dtype=torch.float32, device=device) for _ in range(rotate)]
-    rows = [cfg.m] * world
+    ycer = [torch.empty(m_local, dtype=torch.float32, device=device) for _ in range(rotate)]
+    ycser = [torch.empty(m_local, dtype=torch.float32, device=device) for _ in range(rotate)]
+    if strong:
+        del wt
+        torch.cuda.empty_cache()
 
     sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     if world == 1:
@@ -491,7 +505,18 @@ def run_ours(args):
         secs = start.elapsed_time(end) / 1e3
     secs = max_over_ranks(secs, world, device)
     t_step = secs / args.steps
-    value = world * step_bytes / t_step / 1e9
+    if strong:  # bytes of the whole matrix (every rank's block) per step
+        if world > 1:
+            import torch.distributed as dist
+
+            tb = torch.tensor([step_bytes], dtype=torch.int64, device=device)
+            dist.all_reduce(tb)
+            total_bytes = int(tb.item())
+        else:
+            total_bytes = step_bytes
+    else:
+        total_bytes = world * step_bytes
+    value = total_bytes / t_step / 1e9
 
     # ---- e2e through the public numpy API (H2D of x, D2H of y inside the region)
     e2e_steps = max(3, min(args.steps, args.e2e_steps))
@@ -516,7 +541,7 @@ def run_ours(args):
     e2e_secs = max_over_ranks(time.perf_counter() - t0, world, device)
     e2e_t = e2e_secs / e2e_steps
     h2d = 2 * x_host.size * 4
-    d2h = 2 * cfg.m * world * 4
+    d2h = 2 * cfg.m * (1 if strong else world) * 4
 
     result = None
     if rank == 0:
@@ -524,7 +549,8 @@ def run_ours(args):
         # CPU baseline: the reference's numpy algorithm on this host, bounded sample
         cpu_t, port_encs = cpu_baseline_sample(w, x_host, repeats=args.cpu_repeats)
         cpu_bytes = sum(port_bytes(e, 1) for e in port_encs)
-        assert cpu_bytes == step_bytes, (cpu_bytes, step_bytes)
+        if not strong:
+            assert cpu_bytes == step_bytes, (cpu_bytes, step_bytes)
         cases = []
         if args.cases == "all" and world == 1:
             plan = [("alexnet-fc6", 64), ("vgg-fc6", 1), ("vgg-fc6", 128), ("resnet-conv", 1),
@@ -534,7 +560,8 @@ def run_ours(args):
                 if name == "large":
                     steps_c = 20 if b == 1 else 3
                 cases.append(measure_case(cd, torch, name, b, steps_c, 3, args.seed, device))
-        libs = library_baseline_times(torch, wt, x_host, device) if (args.cases == "all" and world == 1) else {}
+        libs = (library_baseline_times(torch, wt, x_host, device)
+                if (args.cases == "all" and world == 1 and not strong) else {})
         fmt_b = {"cer": cd.storage_bits(cer) // 8, "cser": cd.storage_bits(cser) // 8}
         traffic = _ncu_traffic(cfg.name)
         result = {
@@ -546,13 +573,15 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": round(t_step * 1e3, 5),
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None,
             "dtype": "f32",
-            "data": "synthetic (seeded stand-in for the pretrained AlexNet fc6 layer; SURVEY.md §8(d))",
+            "data": ("synthetic (config 5, drawn on the device per row block; SURVEY.md §8(d))" if strong else
+                     "synthetic (seeded stand-in for the pretrained AlexNet fc6 layer; SURVEY.md §8(d))"),
             "config": {
                 "workload": f"{cfg.name} {cfg.m}x{cfg.n} K={cfg.k} p0={cfg.p_zero}: CER + CSER mat-vec (B=1) per "
-                            f"step, {world} row block(s) of {cfg.m} rows",
+                            f"step, {world} row block(s) of {m_local} rows"
+                            + (" (one matrix row-sharded over the ranks)" if strong else " (one block per rank)"),
                 "l2": f"inputs larger than L2: {rotate} rotating encoded copies "
                       f"({rotate * per_copy / 2**20:.0f} MiB > 126 MiB L2)",
                 "alg_bytes_per_step": step_bytes,
@@ -562,7 +591,7 @@ def run_ours(args):
                 "timing": "CUDA graphs of rotating steps, CUDA events around exactly K steps" if world == 1
                           else "eager, CUDA events, max over ranks",
             },
-            "gmacs": round(world * 2 * cfg.m * cfg.n / t_step / 1e9, 1),
+            "gmacs": round((1 if strong else world) * 2 * cfg.m * cfg.n / t_step / 1e9, 1),
             "roofline": {
                 "bound": "hbm", "kernel": "k_matvec<u16,u32,CER|CSER,896 threads> (the CER and CSER mat-vec)",
                 "achieved": round(step_bytes / t_step / 1e9, 2), "peak": peak, "unit": "GB/s",
@@ -571,17 +600,18 @@ def run_ours(args):
                 "peak_source": peak_src,
                 "per_launch_bytes": {"cer": alg_bytes(cer, 1), "cser": alg_bytes(cser, 1)},
             },
-            "e2e": {"value": round(world * step_bytes / e2e_t / 1e9, 3), "unit": "GB/s",
+            "e2e": {"value": round(total_bytes / e2e_t / 1e9, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_t * 1e3, 4),
                     "api": "paper_1805_10692_b200.dot(enc, numpy x) -> numpy y (pinned staging)"},
             "cpu_baseline": {"value": round(cpu_bytes / cpu_t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
                              "ms_per_step": round(cpu_t * 1e3, 3),
                              "sample": f"oracle/numpy_port (reference lemt numpy path, bitwise-pinned): CER+CSER "
-                                       f"mat-vec on the full {cfg.name} layer, 1 warm-up + median of "
+                                       f"mat-vec on {'rows [0, 256) of' if strong else 'the full'} {cfg.name} layer, "
+                                       f"1 warm-up + median of "
                                        f"{args.cpu_repeats}, single thread (as the reference)",
                              "host_cores": os.cpu_count()},
             "conversion": {"cer_s": round(t_enc_cer, 5), "cser_s": round(t_enc_cser, 5),
-                           "dense_input_gbs": round(w.nbytes / t_enc_cer / 1e9, 2)},
+                           "dense_input_gbs": round(m_local * cfg.n * 4 / t_enc_cer / 1e9, 2)},
             "clocks": clocks,
             "gpu_launches": 2 * args.steps,
             "library_baselines": libs,
