@@ -1,5 +1,6 @@
 """Print per-CTA phase timestamps of the window mat-vec (CERDOT_TRACE=1), relative to the earliest start.
 
+Usage: python tools/trace_matvec.py [config:rows:kind ...]   (default alexnet-fc6:4096:cer/cser)
 Needs a library built with -DCERDOT_TRACE_KERNELS (NVCC_EXTRA=-DCERDOT_TRACE_KERNELS python -m paper_1805_10692_b200.build --force).
 """
 import os, re, subprocess, sys
@@ -18,7 +19,8 @@ torch.cuda.synchronize()
 os.environ["CERDOT_TRACE"] = "1"
 cd.dot_device(e, x, out=y); torch.cuda.synchronize()
 '''
-for cfgname, rows, kind in (("alexnet-fc6", 4096, "cer"), ("alexnet-fc6", 4096, "cser")):
+cases = [tuple(a.split(":")) for a in sys.argv[1:]] or [("alexnet-fc6", "4096", "cer"), ("alexnet-fc6", "4096", "cser")]
+for cfgname, rows, kind in cases:
     env = dict(os.environ, CERDOT_MATVEC_PATH="1")
     out = subprocess.run([sys.executable, "-c", code, cfgname, str(rows), kind], capture_output=True, text=True,
                          env=env).stdout
