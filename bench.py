@@ -472,7 +472,17 @@ def run_ours(args):
 
             shard_cer = [PeerRowShardedDot(c, rows, batch=1) for c in cers]
             shard_cser = [PeerRowShardedDot(c, rows, batch=1) for c in csers]
-            exchange = "fused: cerdot_dot_peers epilogue stores to every rank's symmetric-memory buffer + one barrier"
+            # check the fused exchange against the NCCL all-gather once (same local kernels: bitwise)
+            y_fused = shard_cer[0](xdev[0]).clone()
+            y_nccl = RowShardedDot(cers[0], rows)(xdev[0])
+            ok = torch.tensor([1 if torch.equal(y_fused, y_nccl) else 0], device=device)
+            import torch.distributed as dist
+
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) != 1:
+                raise RuntimeError("fused exchange disagrees with the NCCL all-gather")
+            exchange = ("fused: cerdot_dot_peers epilogue stores to every rank's symmetric-memory buffer + one "
+                        "barrier (checked bitwise against the NCCL all-gather)")
 
             def sharded_step(i):
                 shard_cer[i % rotate](xdev[i % rotate], barrier=False)
