@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
   const int kv = static_cast<int>(min64(a.k, kSmemValues));
   const double wd0 = static_cast<int>(threadIdx.x) < kv ? __ldg(a.omega + threadIdx.x) : 0.0;
 #ifdef CERDOT_TRACE_KERNELS
-  unsigned long long tr[7] = {gtimer(), 0, 0, 0, 0, 0, 0};
+  unsigned long long tr[9] = {gtimer(), 0, 0, 0, 0, 0, 0, 0, 0};
 #define CERDOT_TR(i, dep) \
   if (a.dbg && tr[i] == 0) tr[i] = gtimer() + (dep)
 #else
@@ -641,6 +641,9 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
       for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
       if (lane == 0) put_y(a, y, w.row, a.bg != 0.0 ? static_cast<float>(static_cast<double>(r) + a.bg * a.colsum[0]) : r);
       next_emit = w.row + 1;
+#ifdef CERDOT_TRACE_KERNELS
+      if (a.dbg) tr[7] = gtimer();
+#endif
     }
   };
   if (NBUF > 1) {  // three windows in flight, statically rolled (no register moves)
@@ -663,12 +666,16 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
   }
   emit_empty(R1);
   cp_async_wait<0>();
+#ifdef CERDOT_TRACE_KERNELS
+  if (a.dbg) tr[8] = gtimer();
+#endif
   if (x_async && threadIdx.x == 0) mbar_wait(xbar, 0);  // the CTA must not retire with the x copy in flight
 #ifdef CERDOT_TRACE_KERNELS
   if (a.dbg && lane == 0 && (blockIdx.x % 37) == 0 && (wid == 0 || wid == kWarps - 1)) {
     tr[4] = gtimer();
-    printf("TRACE cta %d warp %d rows %u start %llu prologue %llu wait %llu staged %llu end %llu gath %llu seg %llu\n",
-           blockIdx.x, wid, R1 - R0, tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[6]);
+    printf("TRACE cta %d warp %d rows %u start %llu prologue %llu wait %llu staged %llu end %llu gath %llu seg %llu "
+           "rowdone %llu drained %llu\n",
+           blockIdx.x, wid, R1 - R0, tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[6], tr[7], tr[8]);
   }
 #endif
 }

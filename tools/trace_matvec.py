@@ -24,10 +24,10 @@ for cfgname, rows, kind in cases:
     env = dict(os.environ, CERDOT_MATVEC_PATH="1")
     out = subprocess.run([sys.executable, "-c", code, cfgname, str(rows), kind], capture_output=True, text=True,
                          env=env).stdout
-    recs = [list(map(int, re.findall(r"(\d+)", l)[:10])) for l in out.splitlines() if l.startswith("TRACE")]
+    recs = [list(map(int, re.findall(r"(\d+)", l)[:12])) for l in out.splitlines() if l.startswith("TRACE")]
     if not recs:
         print(out); continue
     t0 = min(r[3] for r in recs)
-    print(f"== {cfgname} rows={rows} {kind}: us since first CTA start: start / prologue / after-wait / x-staged / end / gather+scan done / segments done")
+    print(f"== {cfgname} rows={rows} {kind}: us since first CTA start: start / prologue / after-wait / x-staged / end / gather+scan done / segments done / row written / cp.async drained")
     for r in recs:
-        print(f"cta {r[0]:3d} warp {r[1]:2d} rows {r[2]}: " + " ".join(f"{(v - t0) / 1e3:7.2f}" for v in r[3:10]))
+        print(f"cta {r[0]:3d} warp {r[1]:2d} rows {r[2]}: " + " ".join(f"{(v - t0) / 1e3:7.2f}" for v in r[3:12]))
