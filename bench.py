@@ -609,6 +609,11 @@ def run_ours(args):
                 "traffic_per_launch": traffic.get("per_launch"), "traffic_source": traffic.get("source"),
                 "peak_source": peak_src,
                 "per_launch_bytes": {"cer": alg_bytes(cer, 1), "cser": alg_bytes(cser, 1)},
+                "limiter": ("latency + the shared-memory pipe, not HBM: ~2.5 us of each ~7 us call pass before the "
+                            "first gather (index chain, x staging), ~3 us are random x gathers from shared memory "
+                            "(~3.4 bank-conflict ways) and segment lookups (DESIGN.md §3, tools/trace_matvec.py)"
+                            if not strong else
+                            "the L1/shared data pipe (93% in ncu): x gathers + the colI ring (DESIGN.md §3)"),
             },
             "e2e": {"value": round(total_bytes / e2e_t / 1e9, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_t * 1e3, 4),
