@@ -108,6 +108,16 @@ def test_row_sharded_dot_world2(tmp_path, kind, balanced):
     assert np.array_equal(np.load(out), ref)
 
 
+def test_row_sharded_dot_world3_uneven(tmp_path):
+    """Three ranks, byte-balanced blocks of unequal heights (all-gather of padded blocks), CSER."""
+    out = str(tmp_path / "y3.npy")
+    mp.spawn(_worker, args=(3, _free_port(), "cser", True, out), nprocs=3, join=True)
+    w, xs = synth.make_layer("oracle")
+    x = np.stack([xs[1], -xs[1], 2 * xs[1]], axis=1).astype(np.float64)
+    ref = c_oracle.dot(_as_dict(_host_encoding("cser", w)), x)
+    assert np.array_equal(np.load(out), ref)
+
+
 def test_slices_are_valid_encodings():
     w, xs = synth.make_layer("oracle")
     for kind in ("cer", "cser"):
