@@ -399,7 +399,7 @@ def _clone(cd, enc):
     dev = enc.device_encoding()
     import dataclasses
 
-    new = dataclasses.replace(dev, arena=dev.arena.clone(), _struct=None)
+    new = dataclasses.replace(dev, arena=dev.arena.clone(), _struct=None, _tile_views={})
     cls = type(enc)
     if isinstance(enc, cd.CserMatrix):
         return cls(None, None, None, None, None, enc.m, enc.n, enc.element_bits, enc.mode_index, _device=new)

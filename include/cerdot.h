@@ -19,6 +19,8 @@
  *       new: contiguous row blocks balanced by encoded bytes
  *   cerdot_row_entries
  *       new: derived per-row entry offsets (shortens the mat-vec start-up chain)
+ *   cerdot_tile_view_rows / cerdot_tile_view_build
+ *       new: derived column-tiled view feeding the TMA-staged mat-mat
  *
  * Conventions
  *   - Every pointer marked (device) is CUDA device memory on the current
@@ -46,7 +48,7 @@
 extern "C" {
 #endif
 
-#define CERDOT_ABI_VERSION 1
+#define CERDOT_ABI_VERSION 2
 
 typedef enum {
   CERDOT_OK = 0,
@@ -86,6 +88,13 @@ typedef struct {
                                  (cerdot_row_entries); NULL = the kernels derive them.  A derived index,
                                  not part of the format: it removes one dependent DRAM load from the
                                  mat-vec's start-up chain */
+  /* Optional column-tiled view for the mat-mat (batch > 1), built by cerdot_tile_view_build for
+   * tile_rows = cerdot_tile_view_rows(a, batch); all three zero/NULL = no view (the mat-mat then
+   * gathers X rows from L2).  A derived index, not part of the format. */
+  int32_t tile_rows;          /* X rows per tile (NT) the view was built for */
+  int32_t reserved0;
+  const uint32_t *tile_ptr;   /* (device) T*m+1 u32, T = ceil(n/NT): tile-major row starts of the records */
+  const void *tile_rec;       /* (device) nnz 8-byte records {column in tile | fragment end, fp32 value} */
 } cerdot_matrix;
 
 /* Result of phase 1 of the conversion. */
@@ -173,6 +182,35 @@ int cerdot_dot_host(const cerdot_matrix *a, const float *x_host, int64_t ldx, in
 /* Derived index for cerdot_matrix.row_entry: out[r] = omega_ptr[row_ptr[r]] for r in [0, m], u32
  * (device, m+1).  CERDOT_E_VALUE when nnz does not fit 32 bits.  Stream-ordered. */
 int cerdot_row_entries(const cerdot_matrix *a, uint32_t *out, void *stream);
+
+/* Column-tiled view (derived index) for the TMA-staged mat-mat -- the batch > 1 path of
+ * kernels.py:283-301: every segment split at the X-tile boundaries (colI is ascending inside a segment,
+ * formats.py:220).  cerdot_tile_view_rows returns the tile height NT the mat-mat wants for this batch
+ * (0 = the tiled path does not apply: batch 1, nnz >= 2^32).  Buffers: tile_ptr ceil(n/NT)*m+1 u32,
+ * tile_rec nnz*8 bytes, workspace cerdot_tile_view_workspace_bytes.  Needs a->row_entry.
+ * Stream-ordered. */
+int32_t cerdot_tile_view_rows(const cerdot_matrix *a, int64_t batch);
+size_t cerdot_tile_view_workspace_bytes(const cerdot_matrix *a, int32_t tile_rows);
+int cerdot_tile_view_build(const cerdot_matrix *a, int32_t tile_rows, uint32_t *tile_ptr, void *tile_rec,
+                           void *workspace, size_t workspace_bytes, void *stream);
+
+/* Kernel selection override for A/B measurements and parity tests (process-wide; 0 = automatic, the
+ * default).  Replaces reading environment variables on the dot path.
+ *   CERDOT_PATH_MATVEC: 1 window kernel, 2 CTA-tile kernel, 3 long-row kernel
+ *   CERDOT_PATH_MATMAT: 1 flat L2-gather kernel, 2 per-segment kernel, 3 tiled (needs a view),
+ *                       4 tiled with sum-then-multiply per segment fragment
+ *   CERDOT_PATH_MATVEC_NT: 1 co-resident 16-warp window kernel, 896 the 28-warp one
+ *   CERDOT_PATH_MATMAT_DEPTH: X-row loads in flight of the flat kernel (8 / 16)
+ * Returns the previous value; CERDOT_E_VALUE for an unknown op. */
+typedef enum {
+  CERDOT_PATH_MATVEC = 0,
+  CERDOT_PATH_MATMAT = 1,
+  CERDOT_PATH_MATVEC_NT = 2,
+  CERDOT_PATH_MATMAT_DEPTH = 3,
+  CERDOT_PATH_TRACE = 4,
+  CERDOT_PATH_COUNT
+} cerdot_path_op;
+int32_t cerdot_set_kernel_path(int32_t op, int32_t path);
 
 /* Structural validation of an (untrusted) encoding on the device -- lemt.formats.validate
  * (formats.py:298-392) for the index arrays.  The checks run in the reference's order; the first

@@ -48,6 +48,10 @@ class CerdotMatrix(ctypes.Structure):
         ("max_row_nnz", ctypes.c_int64),
         ("max_row_segments", ctypes.c_int64),
         ("row_entry", ctypes.c_void_p),
+        ("tile_rows", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
+        ("tile_ptr", ctypes.c_void_p),
+        ("tile_rec", ctypes.c_void_p),
     ]
 
 
@@ -98,7 +102,17 @@ _SIGNATURES = {
     "cerdot_dot_host": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _SZ, _P]),
     "cerdot_row_entries": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _P]),
     "cerdot_shard_plan": (ctypes.c_int, [_P, _I32, _P, _I32, _I32, _I64, _I32, ctypes.POINTER(ctypes.c_int64)]),
+    "cerdot_tile_view_rows": (_I32, [ctypes.POINTER(CerdotMatrix), _I64]),
+    "cerdot_tile_view_workspace_bytes": (_SZ, [ctypes.POINTER(CerdotMatrix), _I32]),
+    "cerdot_tile_view_build": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _I32, _P, _P, _P, _SZ, _P]),
+    "cerdot_set_kernel_path": (_I32, [_I32, _I32]),
 }
+
+# cerdot_path_op
+PATH_OPS = {"matvec": 0, "matmat": 1, "matvec_nt": 2, "matmat_depth": 3, "trace": 4}
+# named kernel choices per op (the integers of include/cerdot.h)
+PATH_NAMES = {"matvec": {"auto": 0, "window": 1, "tile": 2, "run": 3},
+              "matmat": {"auto": 0, "flat": 1, "segment": 2, "tiled": 3, "tiled_frag": 4}}
 
 _lib = None
 
@@ -121,10 +135,28 @@ def lib() -> ctypes.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.cerdot_abi_version() != 1:
+        if L.cerdot_abi_version() != 2:
             raise ImportError("libcerdot ABI version mismatch")
         _lib = L
     return _lib
+
+
+class force_path:
+    """Context manager: pin a kernel choice (cerdot_set_kernel_path) for A/B timing and parity tests,
+    e.g. ``with force_path("matvec", "run"): ...``.  Process-wide; restores the previous value."""
+
+    def __init__(self, op: str, path):
+        self.op = PATH_OPS[op]
+        self.path = PATH_NAMES.get(op, {}).get(path, path) if isinstance(path, str) else int(path)
+        self.prev = None
+
+    def __enter__(self):
+        self.prev = lib().cerdot_set_kernel_path(self.op, int(self.path))
+        return self
+
+    def __exit__(self, *exc):
+        lib().cerdot_set_kernel_path(self.op, self.prev)
+        return False
 
 
 def last_error() -> str:

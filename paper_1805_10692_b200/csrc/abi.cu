@@ -8,6 +8,9 @@
 #include "cerdot.h"
 #include "common.cuh"
 #include "encode.cuh"
+#include "tileview.cuh"
+
+#include <atomic>
 
 namespace cerdot {
 
@@ -59,9 +62,15 @@ static int check_matrix(const cerdot_matrix *a, int64_t batch, const float *x, c
     return fail(CERDOT_E_VALUE, "index bits must be one of (8, 16, 32)");
   if (batch < 0) return fail(CERDOT_E_VALUE, "batch must be >= 0");
   if (batch > 1 && (ldx < batch || ldy < batch)) return fail(CERDOT_E_VALUE, "row strides must be >= batch");
+  // the mat-vec kernels read x and write y contiguously: a strided single column must be made contiguous
+  if (batch == 1 && (ldx != 1 || ldy != 1)) return fail(CERDOT_E_VALUE, "batch 1 needs unit row strides");
   if (a->m > 0 && batch > 0 && (x == nullptr || y == nullptr)) return fail(CERDOT_E_VALUE, "null x or y");
   return CERDOT_OK;
 }
+
+static std::atomic<int> g_paths[CERDOT_PATH_COUNT];
+
+int kernel_path(int op) { return (op >= 0 && op < CERDOT_PATH_COUNT) ? g_paths[op].load(std::memory_order_relaxed) : 0; }
 
 }  // namespace cerdot
 
@@ -243,6 +252,33 @@ int cerdot_row_entries(const cerdot_matrix *a, uint32_t *out, void *stream) {
   if (out == nullptr) return fail(CERDOT_E_VALUE, "null row_entry output");
   if (a->m < 0) return fail(CERDOT_E_VALUE, "m must be >= 0");
   return cerdot::row_entries(a, out, static_cast<cudaStream_t>(stream));
+}
+
+int32_t cerdot_set_kernel_path(int32_t op, int32_t path) {
+  if (op < 0 || op >= CERDOT_PATH_COUNT) {
+    fail(CERDOT_E_VALUE, "unknown kernel-path op " + std::to_string(op));
+    return -1;
+  }
+  return g_paths[op].exchange(path);
+}
+
+int32_t cerdot_tile_view_rows(const cerdot_matrix *a, int64_t batch) {
+  if (a == nullptr || a->m <= 0 || a->n <= 0) return 0;
+  return cerdot::tile_view_rows(a, batch);
+}
+
+size_t cerdot_tile_view_workspace_bytes(const cerdot_matrix *a, int32_t tile_rows) {
+  if (a == nullptr || tile_rows <= 0) return 0;
+  return cerdot::tile_view_workspace_bytes(a->m, a->n, tile_rows);
+}
+
+int cerdot_tile_view_build(const cerdot_matrix *a, int32_t tile_rows, uint32_t *tile_ptr, void *tile_rec,
+                           void *workspace, size_t workspace_bytes, void *stream) {
+  int rc = check_matrix(a, 0, nullptr, nullptr, 0, 0);
+  if (rc) return rc;
+  if (tile_ptr == nullptr || (a->nnz > 0 && tile_rec == nullptr)) return fail(CERDOT_E_VALUE, "null tile view buffer");
+  return cerdot::tile_view_build(a, tile_rows, tile_ptr, tile_rec, workspace, workspace_bytes,
+                                 static_cast<cudaStream_t>(stream));
 }
 
 int cerdot_shard_plan(const void *row_ptr, int32_t row_ptr_bits, const void *omega_ptr, int32_t omega_ptr_bits,

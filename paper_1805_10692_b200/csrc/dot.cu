@@ -43,6 +43,7 @@
 
 #include "common.cuh"
 #include "encode.cuh"
+#include "tileview.cuh"
 
 namespace cerdot {
 
@@ -1672,7 +1673,7 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
   }
   if (batch == 1) {
     // rows that fit a tile (known from the encoding's row statistics): CTA-tile TMA pipeline
-    const char *force_path = getenv("CERDOT_MATVEC_PATH");
+    const int force_path = kernel_path(CERDOT_PATH_MATVEC);
     const bool tile_ok = a.max_row_nnz > 0 && a.max_row_nnz <= kTileE && a.max_row_segs <= kTileS &&
                          a.k <= kSmemValues &&
                          tile_layout(a.k, a.n, sizeof(ColT), sizeof(PtrT), CSER ? a.oi_bits / 8 : 1).total <=
@@ -1683,7 +1684,7 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
     // long rows (>= 4096 entries on average, the 32768^2 layer: 9829): the 32-warp run kernel
     // (431 -> 314 us there); at ~1000-entry rows (AlexNet, VGG fc6) the window kernel is 0-30% faster
     const bool long_rows = a.nnz >= int64_t(4096) * a.m;
-    const int want = force_path ? atoi(force_path) : (few_rows ? 2 : (long_rows ? 3 : 1));
+    const int want = force_path ? force_path : (few_rows ? 2 : (long_rows ? 3 : 1));
     if (tile_ok && want == 2) return launch_matvec_tile<ColT, PtrT, CSER>(a, x, y, st);
     if (want == 3 && run_layout(a.k, a.n, kRunNT / 32, RunRing<ColT>::kDepth).total <= static_cast<uint32_t>(kMaxSmemBytes))
       return launch_matvec_run<ColT, PtrT, CSER>(a, x, y, st);
@@ -1692,9 +1693,8 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
     // index prologue (rowPtr -> omegaPtr -> colI latency chain) overlaps this call's work.
     const uint32_t oib = CSER ? static_cast<uint32_t>(a.oi_bits / 8) : 1u;
     // (measured: AlexNet-fc6 12.5 us co-resident vs 10.6 us exclusive -- the post-wait chain dominates,
-    // so the co-resident variant is opt-in: CERDOT_MATVEC_NT=1)
-    const char *force = getenv("CERDOT_MATVEC_NT");
-    const int want_nt = force ? atoi(force) : 0;
+    // so the co-resident variant is opt-in: CERDOT_PATH_MATVEC_NT = 1)
+    const int want_nt = kernel_path(CERDOT_PATH_MATVEC_NT);
     if (want_nt == 1 && matvec_smem(a.k, a.n, true, 16, 3, oib) <= kHalfSmemBytes)
       return launch_matvec<ColT, PtrT, CSER, true, 512, 1, 2, 3>(a, x, y, st);
     // 28 warps per SM (896 threads, <= 72 regs) when x and the per-warp tables fit: enough warps that
@@ -1716,8 +1716,7 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
   const bool al2 = (ldx % 2 == 0) && (reinterpret_cast<uintptr_t>(x) % 8 == 0);
   const int V = (batch > 64 && al4) ? 4 : ((batch > 32 && al2) ? 2 : 1);
   const int64_t units = a.m * ceil_div(batch, 32 * V);
-  const char *mm_path = getenv("CERDOT_MM_PATH");
-  if (!mm_path || atoi(mm_path) != 0) {
+  if (kernel_path(CERDOT_PATH_MATMAT) != 2) {
     // flat entry stream (default); one resident wave of CTAs (occupancy API), units round-robin over warps
     auto go = [&](auto kern) -> int {
       int per_sm = 0;
@@ -1731,13 +1730,13 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
     // 8 X-row loads in flight for every V (measured: V = 4 at D = 4 runs 3 CTAs per SM instead of 2
     // but is slower on all of VGG fc6 B=128, ResNet conv B=1568 and 32768^2 B=256)
     // V = 2 at 16 loads in flight (AlexNet fc6 B=64: 97 -> 80 us); V = 1 stays at 8 (16 is 9% slower at
-    // B=32).  CERDOT_MM_D forces 8 / 16 for V <= 2 (A/B only).
-    const char *fd = getenv("CERDOT_MM_D");
+    // B=32).  CERDOT_PATH_MATMAT_DEPTH forces 8 / 16 for V <= 2 (A/B only).
+    const int fd = kernel_path(CERDOT_PATH_MATMAT_DEPTH);
     if (V == 4) return go(k_matmat_flat<ColT, PtrT, CSER, 4, 8>);
     if (V == 2)
-      return (fd ? atoi(fd) : 16) == 16 ? go(k_matmat_flat<ColT, PtrT, CSER, 2, 16>)
+      return (fd ? fd : 16) == 16 ? go(k_matmat_flat<ColT, PtrT, CSER, 2, 16>)
                                         : go(k_matmat_flat<ColT, PtrT, CSER, 2, 8>);
-    return (fd ? atoi(fd) : 8) == 16 ? go(k_matmat_flat<ColT, PtrT, CSER, 1, 16>)
+    return (fd ? fd : 8) == 16 ? go(k_matmat_flat<ColT, PtrT, CSER, 1, 16>)
                                      : go(k_matmat_flat<ColT, PtrT, CSER, 1, 8>);
   }
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(units, 8),
@@ -1822,7 +1821,7 @@ int dot(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, fl
   a.segs = mat->segments;
   a.max_row_nnz = mat->max_row_nnz;
   a.nnz = mat->nnz;
-  a.dbg = getenv("CERDOT_TRACE") ? 1 : 0;
+  a.dbg = kernel_path(CERDOT_PATH_TRACE) ? 1 : 0;
   a.max_row_segs = mat->max_row_segments;
   a.re = mat->row_entry;
   if (a.m == 0 || batch == 0) return CERDOT_OK;
@@ -1841,6 +1840,13 @@ int dot(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, fl
     }
     CERDOT_LAUNCH_CHECK();
     a.colsum = cs;
+  }
+  // batch > 1: the TMA-staged mat-mat over the column-tiled view when the matrix carries one
+  const int mm = kernel_path(CERDOT_PATH_MATMAT);
+  if (batch > 1 && (mm == 0 || mm == 3 || mm == 4)) {
+    bool used = false;
+    if (int rc = matmat_tiled(mat, x, ldx, batch, y, ldy, a.colsum, peers, a.npeer, peer_offset, st, &used)) return rc;
+    if (used) return CERDOT_OK;
   }
   return cser ? by_col<true>(a, mat->col_bits, mat->omega_ptr_bits, x, ldx, batch, y, ldy, st)
               : by_col<false>(a, mat->col_bits, mat->omega_ptr_bits, x, ldx, batch, y, ldy, st);

@@ -57,6 +57,12 @@ def stream_ptr(device=None) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+def ctypes_copy(dst, src) -> None:
+    import ctypes
+
+    ctypes.memmove(ctypes.addressof(dst), ctypes.addressof(src), ctypes.sizeof(src))
+
+
 def _align(v: int) -> int:
     return (v + _ALIGN - 1) // _ALIGN * _ALIGN
 
@@ -78,6 +84,7 @@ class DeviceEncoding:
     max_row_segments: int = 0  # largest row in segments (0 = unknown)
     _struct: object = field(default=None, repr=False)
     _row_entry_ready: bool = False
+    _tile_views: dict = field(default_factory=dict, repr=False)  # NT -> (tile_ptr, tile_rec, struct)
 
     def fill_row_entries(self, stream: int) -> None:
         """Compute the derived rowEntry index on the device (stream-ordered)."""
@@ -88,6 +95,38 @@ class DeviceEncoding:
         _native.check(_native.lib().cerdot_row_entries(self.struct(), self.ptr("rowEntry"), stream))
         self._row_entry_ready = True
         self._struct = None
+
+    def tile_struct(self, batch: int, stream: int):
+        """The matrix struct carrying the column-tiled view the mat-mat wants at this batch (built on the
+        device on first use, stream-ordered, then cached), or the plain struct when no view applies."""
+        base = self.struct()
+        if batch <= 1 or base.row_entry is None:
+            return base
+        L = _native.lib()
+        nt = int(L.cerdot_tile_view_rows(base, batch))
+        if nt <= 0:
+            return base
+        hit = self._tile_views.get(nt)
+        if hit is None:
+            torch = torch_mod()
+            tiles = -(-self.n // nt)
+            tptr = torch.empty(tiles * self.m + 1, dtype=torch.int32, device=self.device)
+            rec = torch.empty(max(1, self.nnz) * 2, dtype=torch.int32, device=self.device)
+            ws = torch.empty(max(256, int(L.cerdot_tile_view_workspace_bytes(base, nt))), dtype=torch.uint8,
+                             device=self.device)
+            _native.check(L.cerdot_tile_view_build(base, nt, tptr.data_ptr(), rec.data_ptr(), ws.data_ptr(),
+                                                   ws.numel(), stream))
+            s = _native.CerdotMatrix()
+            ctypes_copy(s, base)
+            s.tile_rows, s.tile_ptr, s.tile_rec = nt, tptr.data_ptr(), rec.data_ptr()
+            hit = (tptr, rec, s, ws)  # ws kept alive until the build has run (stream-ordered)
+            self._tile_views[nt] = hit
+        return hit[2]
+
+    @property
+    def tile_view_bytes(self) -> int:
+        """Device bytes held by the cached column-tiled views (derived indices)."""
+        return sum(v[0].numel() * 4 + v[1].numel() * 4 for v in self._tile_views.values())
 
     @staticmethod
     def layout(kind: int, m: int, k: int, nnz: int, segments: int, bits: dict):

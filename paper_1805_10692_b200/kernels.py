@@ -192,65 +192,80 @@ def row_trace(a, row: int, input_bits: int = 32, output_bits: int | None = None)
 # --------------------------------------------------------------------------- numeric kernels
 
 
-class _Workspace:
-    """Per-device scratch for the background column sums (no allocation on the hot path)."""
-
-    def __init__(self):
-        self._buf = {}
-
-    def get(self, device, nbytes: int):
-        torch = torch_mod()
-        key = (device.type, device.index)
-        buf = self._buf.get(key)
-        if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
-            self._buf[key] = buf
-        return buf
-
-
-_WS = _Workspace()
-
-
+def _check_out(out, m: int, x, batch: int, keep_2d: bool):
+    """Validate a caller-supplied output (kernels write m x batch fp32 through row stride out.stride(0))."""
+    torch = torch_mod()
+    want = (m, batch) if keep_2d else (m,)
+    if not isinstance(out, torch.Tensor) or out.dtype != torch.float32 or out.device != x.device:
+        raise ValueError(f"out must be a float32 tensor on {x.device}")
+    if tuple(out.shape) != want:
+        raise ValueError(f"out has shape {tuple(out.shape)}, expected {want}")
+    if out.stride(-1) != 1 or (out.ndim == 2 and batch == 1 and out.stride(0) != 1) or \
+            (out.ndim == 2 and out.stride(0) < batch):
+        raise ValueError("out must have unit column stride and row stride >= batch")
 
 
 def dot_device(enc, x, out=None, stream=None, peers=None, peer_offset: int = 0):
     """Device-only entry: ``x`` a CUDA fp32 tensor (n,) or (n, B); returns y (m,) / (m, B) fp32.
 
-    Stream-ordered on ``stream`` (default: torch's current stream), no host sync.  ``peers``: a CUDA
-    int64 tensor of other ranks' output-buffer addresses; every y element is then also stored at element
-    ``peer_offset + i`` of each of them from the kernels' epilogue (cerdot_dot_peers, the fused
-    row-sharded all-gather; the caller adds the cross-rank barrier).
+    Stream-ordered on ``stream`` (default: torch's current stream of x's device), no host sync.  The
+    encoding must live on x's device.  ``out`` (optional) must be float32 on that device with y's shape
+    and a unit inner stride.  ``peers``: a CUDA int64 tensor of other ranks' output-buffer addresses;
+    every y element is then also stored at element ``peer_offset + i`` of each of them from the kernels'
+    epilogue (cerdot_dot_peers, the fused row-sharded all-gather; the caller adds the cross-rank barrier).
+    For batch > 1 the dot runs the TMA-staged mat-mat over the encoding's column-tiled view, built on the
+    device on the first mat-mat call for that tile height and cached on the encoding.
     """
     torch = torch_mod()
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise ValueError("dot_device needs a CUDA tensor input")
     dev = enc._dev if enc._dev is not None else enc.device_encoding(x.device)
+    if dev.device != x.device:
+        raise ValueError(f"the encoding lives on {dev.device}, the input on {x.device}")
+    if x.ndim not in (1, 2) or x.shape[0] != dev.n:
+        _check_shape(dev.n, tuple(x.shape))
     if x.dtype != torch.float32:
         x = x.to(torch.float32)
-    if x.ndim == 1:
+    keep_2d = x.ndim == 2
+    batch = int(x.shape[1]) if keep_2d else 1
+    if batch == 1:
+        if x.ndim == 2:
+            x = x.reshape(dev.n)  # an (n, 1) column (a view when its stride allows, else a copy)
         if x.stride(0) != 1:
             x = x.contiguous()
-        batch, ldx = 1, 1
+        ldx = 1
     else:
         if x.stride(1) != 1:
             x = x.contiguous()
-        batch, ldx = int(x.shape[1]), x.stride(0)
-    if x.shape[0] != dev.n or x.ndim > 2:
-        _check_shape(dev.n, tuple(x.shape))
+        ldx = x.stride(0)
     if out is None:
-        out = torch.empty((dev.m,) if batch == 1 else (dev.m, batch), dtype=torch.float32, device=x.device)
-    ldy = 1 if out.ndim == 1 else out.stride(0)
-    st = dev.struct()
-    # == cerdot_dot_workspace_bytes: the column sums (+ 16 row-range partials each when batch > 1)
-    ws_bytes = (8 * batch * (17 if batch > 1 else 1)) if dev.background != 0.0 else 0
-    ws_ptr = _WS.get(x.device, ws_bytes).data_ptr() if ws_bytes else None
-    sp = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
-    if peers is not None and peers.numel() > 0:
-        if peers.dtype != torch.int64 or peers.device != x.device:
-            raise ValueError("peers must be an int64 tensor of device pointers on the dot's device")
-        _native.check(_native.lib().cerdot_dot_peers(st, x.data_ptr(), ldx, batch, out.data_ptr(), ldy,
-                                                      peers.data_ptr(), int(peers.numel()), int(peer_offset),
-                                                      ws_ptr, ws_bytes, sp))
-        return out
-    _native.check(_native.lib().cerdot_dot(st, x.data_ptr(), ldx, batch, out.data_ptr(), ldy, ws_ptr, ws_bytes, sp))
+        out = torch.empty((dev.m, batch) if keep_2d else (dev.m,), dtype=torch.float32, device=x.device)
+    else:
+        _check_out(out, dev.m, x, batch, keep_2d)
+    ldy = 1 if (out.ndim == 1 or batch == 1) else out.stride(0)
+    with torch.cuda.device(x.device):
+        cur = torch.cuda.current_stream(x.device)
+        sp = stream if stream is not None else cur.cuda_stream
+        st = dev.tile_struct(batch, sp) if batch > 1 else dev.struct()
+        # == cerdot_dot_workspace_bytes: the column sums (+ 16 row-range partials each when batch > 1),
+        # allocated per call from torch's caching allocator (ordered on the current stream; recorded on a
+        # foreign one), so calls on different streams never share scratch
+        ws_bytes = (8 * batch * (17 if batch > 1 else 1)) if dev.background != 0.0 else 0
+        ws = None
+        if ws_bytes:
+            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=x.device)
+            if stream is not None and stream != cur.cuda_stream:
+                ws.record_stream(torch.cuda.ExternalStream(stream, device=x.device))
+        ws_ptr = ws.data_ptr() if ws is not None else None
+        if peers is not None and peers.numel() > 0:
+            if peers.dtype != torch.int64 or peers.device != x.device:
+                raise ValueError("peers must be an int64 tensor of device pointers on the dot's device")
+            _native.check(_native.lib().cerdot_dot_peers(st, x.data_ptr(), ldx, batch, out.data_ptr(), ldy,
+                                                          peers.data_ptr(), int(peers.numel()), int(peer_offset),
+                                                          ws_ptr, ws_bytes, sp))
+            return out
+        _native.check(_native.lib().cerdot_dot(st, x.data_ptr(), ldx, batch, out.data_ptr(), ldy, ws_ptr, ws_bytes,
+                                               sp))
     return out
 
 
@@ -264,7 +279,7 @@ class _HostIO(threading.local):
 
     def get(self, m: int, n: int, batch: int, ws_bytes: int):
         torch = torch_mod()
-        if self.dev is None or torch._C._cuda_getDevice() != self.dev.index:
+        if self.dev is None:
             self.dev = require_cuda()
             self.sets = {}
         key = (m, n, batch)
@@ -286,13 +301,16 @@ _IO = _HostIO()
 
 
 def _dot_host(a, xv: np.ndarray) -> np.ndarray:
-    """numpy x -> pinned staging -> one C call (cerdot_dot_host: H2D, kernel, D2H, sync) -> float64 numpy."""
+    """numpy x -> pinned staging -> one C call (cerdot_dot_host: H2D, kernel, D2H, sync) -> float64 numpy
+    of the reference's shape ((m,) for a vector, (m, B) for a matrix, including B = 1)."""
     torch = torch_mod()
     batch = 1 if xv.ndim == 1 else int(xv.shape[1])
     if _IO.dev is None:
         _IO.dev = require_cuda()
     dev = a._dev if a._dev is not None else a.device_encoding(_IO.dev)
-    st = dev.struct()
+    if dev.device != _IO.dev:  # run where the encoding lives
+        _IO.dev, _IO.sets = dev.device, {}
+    st = dev.tile_struct(batch, torch._C._cuda_getCurrentRawStream(_IO.dev.index)) if batch > 1 else dev.struct()
     L = _native.lib()
     key = (a.m, a.n, batch, st.background != 0.0)  # what the workspace size depends on
     ws_bytes = _IO.ws_bytes.get(key)
@@ -302,10 +320,12 @@ def _dot_host(a, xv: np.ndarray) -> np.ndarray:
             _IO.ws_bytes.clear()
         _IO.ws_bytes[key] = ws_bytes
     px, px_np, py, py_np, ws = _IO.get(a.m, a.n, batch, ws_bytes)
-    np.copyto(px_np, xv, casting="unsafe")  # the kernels compute in fp32
-    _native.check(L.cerdot_dot_host(st, px.data_ptr(), batch, batch, py.data_ptr(), batch, ws.data_ptr(),
-                                    ws.numel(), torch._C._cuda_getCurrentRawStream(_IO.dev.index)))
-    return py_np.astype(np.float64)
+    np.copyto(px_np, xv.reshape(px_np.shape), casting="unsafe")  # the kernels compute in fp32
+    with torch.cuda.device(_IO.dev):
+        _native.check(L.cerdot_dot_host(st, px.data_ptr(), batch, batch, py.data_ptr(), batch, ws.data_ptr(),
+                                        ws.numel(), torch._C._cuda_getCurrentRawStream(_IO.dev.index)))
+    y = py_np.astype(np.float64)
+    return y.reshape(a.m, 1) if (xv.ndim == 2 and batch == 1) else y
 
 
 def _dot_encoded(a, x, trace, input_bits, output_bits, tracer):

@@ -102,3 +102,20 @@ def validate_case_arrays(bases, case) -> dict:
 def validate_cases():
     with open(os.path.join(GOLDEN, "validate_cases.json")) as f:
         return json.load(f)
+
+
+@pytest.fixture
+def kernel_path():
+    """pin(op, path): force a kernel choice (cerdot_set_kernel_path) for the rest of the test."""
+    from paper_1805_10692_b200 import _native
+
+    pinned = []
+
+    def pin(op, path):
+        ctx = _native.force_path(op, path)
+        ctx.__enter__()
+        pinned.append(ctx)
+
+    yield pin
+    for ctx in reversed(pinned):
+        ctx.__exit__(None, None, None)

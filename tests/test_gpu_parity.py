@@ -153,25 +153,27 @@ def test_full_batch_resnet_conv_properties():
 
 
 @pytest.mark.parametrize("name,batch", [("alexnet-fc6", 64), ("vgg-fc6", 96), ("resnet-conv", 200), ("oracle", 37)])
-def test_matmat_kernels_agree_bitwise(monkeypatch, name, batch):
+def test_matmat_kernels_agree_bitwise(name, batch):
     """The flat entry-stream mat-mat kernel and the per-segment one compute every column in the same
     fp32 order: identical outputs (V = 1, 2, 4; full and partial column chunks; CER and CSER)."""
+    from paper_1805_10692_b200._native import force_path
+
     w, _ = synth.make_layer(name)
     x = torch.from_numpy(np.random.default_rng(2).standard_normal((w.shape[1], batch), dtype=np.float32)).cuda()
     wt = torch.from_numpy(w).cuda()
     for encode in (cd.encode_cer, cd.encode_cser):
         enc = encode(wt)
-        monkeypatch.setenv("CERDOT_MM_PATH", "0")
-        y0 = cd.dot(enc, x)
-        monkeypatch.delenv("CERDOT_MM_PATH")
-        y1 = cd.dot(enc, x)
+        with force_path("matmat", "segment"):
+            y0 = cd.dot(enc, x)
+        with force_path("matmat", "flat"):
+            y1 = cd.dot(enc, x)
         assert torch.equal(y0, y1), (name, encode.__name__)
 
 
 @pytest.mark.parametrize("path", ["1", "2", "3"])
-def test_u32_column_indices(monkeypatch, path):
+def test_u32_column_indices(kernel_path, path):
     """n > 65535 (u32 colI): every mat-vec kernel and the mat-mat kernel, integer alphabet -> bitwise."""
-    monkeypatch.setenv("CERDOT_MATVEC_PATH", path)
+    kernel_path("matvec", int(path))
     rng = np.random.default_rng(31)
     m, n = 40, 70001
     w = rng.choice(np.arange(-3.0, 4.0), size=(m, n), p=[0.02, 0.03, 0.05, 0.8, 0.05, 0.03, 0.02])
@@ -295,9 +297,9 @@ def test_wide_alphabets_up_to_fast_limit():
 
 @pytest.mark.parametrize("path", ["tile", "window", "run"])
 @pytest.mark.parametrize("name", ["oracle", "alexnet-fc6", "resnet-conv"])
-def test_matvec_paths_agree_with_oracle(monkeypatch, config_goldens, name, path):
+def test_matvec_paths_agree_with_oracle(kernel_path, config_goldens, name, path):
     """Every mat-vec kernel (CTA-tile TMA pipeline, warp-window kernel, 32-warp run kernel) meets the bar."""
-    monkeypatch.setenv("CERDOT_MATVEC_PATH", {"window": "1", "tile": "2", "run": "3"}[path])
+    kernel_path("matvec", path)
     meta, ys = config_goldens
     w, _ = synth.make_layer(name)
     x1 = np.random.default_rng(1).standard_normal(w.shape[1], dtype=np.float32)
@@ -308,9 +310,9 @@ def test_matvec_paths_agree_with_oracle(monkeypatch, config_goldens, name, path)
 
 
 @pytest.mark.parametrize("path", ["1", "2", "3"])
-def test_matvec_tile_edge_rows(monkeypatch, path):
+def test_matvec_tile_edge_rows(kernel_path, path):
     """Empty rows, single-entry rows, a long row next to short ones, non-zero background (every kernel)."""
-    monkeypatch.setenv("CERDOT_MATVEC_PATH", path)
+    kernel_path("matvec", int(path))
     rng = np.random.default_rng(9)
     w = np.zeros((300, 700))
     w[5, :] = rng.integers(1, 4, size=700)           # a dense row (700 entries, few segments)
@@ -361,9 +363,9 @@ def test_row_entry_index(name):
         assert np.array_equal(re, enc.omega_ptr.astype(np.int64)[enc.row_ptr.astype(np.int64)])
         assert dev.struct().row_entry
         for path in ("1", "2"):
-            import os
-            os.environ["CERDOT_MATVEC_PATH"] = path
-            try:
+            from paper_1805_10692_b200._native import force_path
+
+            with force_path("matvec", int(path)):
                 y_re = cd.dot_device(enc, x).cpu().numpy()
                 dev._row_entry_ready = False
                 dev._struct = None
@@ -371,8 +373,6 @@ def test_row_entry_index(name):
                 y_plain = cd.dot_device(enc, x).cpu().numpy()
                 dev._row_entry_ready = True
                 dev._struct = None
-            finally:
-                del os.environ["CERDOT_MATVEC_PATH"]
             assert np.array_equal(y_re, y_plain), (name, encode.__name__, path)
 
 

@@ -1,5 +1,6 @@
 """One dot call (mat-vec or mat-mat, for ncu): python tools/mm_one.py config batch kind [calls]; the kernel variant comes from
-CERDOT_MM_PATH.  The first call warms up; profile with --launch-skip accordingly."""
+MM_PATH (auto / flat / segment / tiled) and MV_PATH (auto / window / tile / run), pinned with cerdot_set_kernel_path.
+The first call warms up (and builds the mat-mat's tile view); profile with --launch-skip accordingly."""
 import os
 import sys
 
@@ -9,6 +10,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1805_10692_b200 as cd  # noqa: E402
 from paper_1805_10692_b200 import synth  # noqa: E402
+from paper_1805_10692_b200._native import force_path  # noqa: E402
 
 
 def main():
@@ -24,8 +26,9 @@ def main():
     enc = (cd.encode_cer if kind == "cer" else cd.encode_cser)(w)
     del w
     y = torch.empty((cfg.m, batch) if batch > 1 else (cfg.m,), device="cuda")
-    for _ in range(calls):
-        cd.dot_device(enc, x, out=y)
+    with force_path("matmat", os.environ.get("MM_PATH", "auto")), force_path("matvec", os.environ.get("MV_PATH", "auto")):
+        for _ in range(calls):
+            cd.dot_device(enc, x, out=y)
     torch.cuda.synchronize()
     print("ok", float(y.abs().sum()))
 
