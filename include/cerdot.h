@@ -266,6 +266,14 @@ int cerdot_trace_counts(const cerdot_matrix *a, uint64_t *counts, void *workspac
 int cerdot_lemx_unpack(const void *payload, int32_t element_bits, int64_t k, int64_t omega_offset, double *omega,
                        const int64_t *spans, int32_t count, void *arena, void *stream);
 
+/* Synthetic inputs (benchmark / tests, not the format path): out[i] = levels[searchsorted(cdf, u_{offset+i},
+ * side='right')] for i < count, where u_j is the j-th random() of numpy's Generator(PCG64) whose 128-bit
+ * state / increment are state[0..1] / inc[0..1] (low word first, as numpy's bit_generator.state) -- i.e.
+ * numpy's default_rng(seed).choice(k, size, p) bit for bit, with cdf = cumsum(p)/cumsum(p)[-1] (float64)
+ * and the draw starting `offset` elements in.  cdf / levels / out are device arrays.  Stream-ordered. */
+int cerdot_synth_choice(const uint64_t *state, const uint64_t *inc, uint64_t offset, const double *cdf,
+                        const float *levels, int32_t k, int64_t count, float *out, void *stream);
+
 /* Row-shard planner (host).  row_ptr / omega_ptr are HOST arrays of the
  * given widths.  Writes parts+1 row bounds (bounds[0]=0, bounds[parts]=m)
  * splitting rows into contiguous blocks of near-equal encoded bytes

@@ -106,6 +106,7 @@ _SIGNATURES = {
     "cerdot_tile_view_workspace_bytes": (_SZ, [ctypes.POINTER(CerdotMatrix), _I32]),
     "cerdot_tile_view_build": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _I32, _P, _P, _P, _SZ, _P]),
     "cerdot_set_kernel_path": (_I32, [_I32, _I32]),
+    "cerdot_synth_choice": (ctypes.c_int, [_P, _P, ctypes.c_uint64, _P, _P, _I32, _I64, _P, _P]),
 }
 
 # cerdot_path_op
@@ -132,6 +133,8 @@ def lib() -> ctypes.CDLL:
                 "(there is no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in _SIGNATURES.items():
+            if os.environ.get("CERDOT_LIB") and not hasattr(L, name):
+                continue  # A/B timing against an older build (tools/ab_build.sh): newer entry points absent
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

@@ -254,6 +254,13 @@ int cerdot_row_entries(const cerdot_matrix *a, uint32_t *out, void *stream) {
   return cerdot::row_entries(a, out, static_cast<cudaStream_t>(stream));
 }
 
+int cerdot_synth_choice(const uint64_t *state, const uint64_t *inc, uint64_t offset, const double *cdf,
+                        const float *levels, int32_t k, int64_t count, float *out, void *stream) {
+  if (state == nullptr || inc == nullptr || cdf == nullptr || levels == nullptr || (count > 0 && out == nullptr))
+    return fail(CERDOT_E_VALUE, "synth_choice: null argument");
+  return cerdot::synth_choice(state, inc, offset, cdf, levels, k, count, out, static_cast<cudaStream_t>(stream));
+}
+
 int32_t cerdot_set_kernel_path(int32_t op, int32_t path) {
   if (op < 0 || op >= CERDOT_PATH_COUNT) {
     fail(CERDOT_E_VALUE, "unknown kernel-path op " + std::to_string(op));

@@ -292,7 +292,7 @@ __host__ __device__ __forceinline__ MatvecSmem matvec_layout(int64_t k, int64_t 
   L.bar = take(16u);
   L.wv = take(static_cast<uint32_t>(min64(k, kSmemValues)) * 4u);
   L.pre = take(warps * kWin * 4u);
-  L.off = take(warps * 32u * 4u);
+  L.off = take(warps * 32u * 8u);  // per-warp lane offsets, (hi, lo) fp32 pairs
   L.ring_op = take(warps * depth * 128u);
   L.ring_oi = take(warps * depth * 32u * oi_bytes);
   L.xs = take(static_cast<uint32_t>(n_smem) * 4u);
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
   MatvecSmem L = matvec_layout(a.k, XSMEM ? a.n : 0, kWarps, D, oib);
   float *wv = reinterpret_cast<float *>(smem + L.wv);
   float *pre = reinterpret_cast<float *>(smem + L.pre) + wid * W;
-  float *off = reinterpret_cast<float *>(smem + L.off) + wid * 32;
+  float2 *off = reinterpret_cast<float2 *>(smem + L.off) + wid * 32;
   unsigned char *ring_op = smem + L.ring_op + wid * D * 128;
   unsigned char *ring_oi = smem + L.ring_oi + wid * D * 32 * oib;
   float *xs = reinterpret_cast<float *>(smem + L.xs);
@@ -548,19 +548,34 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
     const float run = (w0 >= w.e0 && wn <= w.e1)
                           ? gather_prefix<ColT, XSMEM, false>(cur, w0, w.e0, w.e1, xs, x, pre, lane)
                           : gather_prefix<ColT, XSMEM, true>(cur, w0, w.e0, w.e1, xs, x, pre, lane);
-    float incl = run;
+    // Lane offsets (exclusive scan of the lane totals), scanned in fp64 and kept as an fp32 pair
+    // hi + lo.  A segment sum is a difference of window-global prefixes G; with all-positive x a plain
+    // fp32 offset (a sum of up to ~1000 entries) cancels against a segment of a few entries and its
+    // rounding dominates (measured: 1.8e-5 on AlexNet fc6 with x = |N(0,1)|).  With the pair, the hi
+    // parts of two nearby prefixes subtract exactly (Sterbenz) and only the fp32 lane-local prefixes
+    // (<= 32 entries) round; per-segment arithmetic stays fp32 (an fp64 G cost 11-21% of the call).
+    double incl = run;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const float t = __shfl_up_sync(0xffffffffu, incl, d);
+      const double t = __shfl_up_sync(0xffffffffu, incl, d);
       if (lane >= d) incl += t;
     }
-    const float excl = __shfl_up_sync(0xffffffffu, incl, 1);
-    off[lane] = lane ? excl : 0.f;
+    {
+      const double up = __shfl_up_sync(0xffffffffu, incl, 1);  // every lane takes part in the shuffle
+      const double excl = lane ? up : 0.0;
+      const float hi = static_cast<float>(excl);
+      off[lane] = make_float2(hi, static_cast<float>(excl - static_cast<double>(hi)));
+    }
     __syncwarp();
-    CERDOT_TR(5, __float_as_uint(excl) & 0u);
-    // window-global inclusive prefix at window position p: lane offset (conflict-free 32-entry table)
-    // plus the lane-local prefix
-    auto G = [&](uint32_t p) { return off[p >> 5] + pre[ppos(p)]; };
+    CERDOT_TR(5, static_cast<uint32_t>(incl) & 0u);
+    // window-global inclusive prefix at window position p as (hi, lo + lane-local prefix)
+    struct GP {
+      float hi, lo;
+    };
+    auto G = [&](uint32_t p) -> GP {
+      const float2 o = off[p >> 5];
+      return GP{o.x, o.y + pre[ppos(p)]};
+    };
     if (!w_ready) {
       mbar_wait(wbar, 0);
       w_ready = true;
@@ -568,19 +583,23 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
     if (single) {
       // ---- the whole row is in this window: lane i of a batch takes segment s0 + 32t + i, reads the
       // window prefix at its end and gets its start value (the previous segment's end) by shuffle
-      float g_prev = 0.f;      // G before the row (the masked gather zeroed entries before e0)
       uint32_t e_prev = w.e0;  // end of the previous segment
+      // segment [st, en): G(en - 1) - G(st - 1), both ends read from the tables by the segment's own lane
+      // (G before the row is 0: the masked gather zeroed the entries before e0)
       auto seg = [&](uint32_t en, int k, bool valid) {
-        const float ge = (valid && en > w0) ? G(en - 1u - w0) : 0.f;
-        float gs = __shfl_up_sync(0xffffffffu, ge, 1);
         uint32_t st = __shfl_up_sync(0xffffffffu, en, 1);
-        if (lane == 0) {
-          gs = g_prev;
-          st = e_prev;
-        }
-        g_prev = __shfl_sync(0xffffffffu, ge, 31);
+        if (lane == 0) st = e_prev;
         e_prev = __shfl_sync(0xffffffffu, en, 31);
-        if (valid && en > st) acc = fmaf(wv[k], ge - gs, acc);
+        if (valid && en > st) {
+          const GP ge = G(en - 1u - w0);
+          float d_hi = ge.hi, d_lo = ge.lo;
+          if (st > w0) {
+            const GP gs = G(st - 1u - w0);
+            d_hi -= gs.hi;
+            d_lo -= gs.lo;
+          }
+          acc = fmaf(wv[k], d_hi + d_lo, acc);
+        }
       };
 #pragma unroll
       for (int i = 0; i < kPre; ++i) {
@@ -617,12 +636,18 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
         const uint32_t b = (en < wn ? en - w0 : W) - 1u;
         const float pb = pre[ppos(b)];
         if (lo == 0u) {
-          total = off[b >> 5] + pb;
+          const float2 ob = off[b >> 5];
+          total = ob.x + (ob.y + pb);
           if (st < w0) total = carry + total;  // the segment continued from the previous window
         } else {
           const uint32_t a0 = lo - 1u;
           const float pa = pre[ppos(a0)];
-          total = ((a0 >> 5) == (b >> 5)) ? pb - pa : (off[b >> 5] + pb) - (off[a0 >> 5] + pa);
+          if ((a0 >> 5) == (b >> 5)) {
+            total = pb - pa;
+          } else {
+            const float2 ob = off[b >> 5], oa = off[a0 >> 5];
+            total = (ob.x - oa.x) + ((ob.y + pb) - (oa.y + pa));
+          }
         }
         if (done) acc = fmaf(wv[CSER ? ring_oi_val(s) : static_cast<int>(s - w.s0 + 1)], total, acc);
       }

@@ -19,6 +19,10 @@ int matmat_tiled(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t 
                  const double *colsum, float *const *peers, int npeers, int64_t peer_offset, cudaStream_t st,
                  bool *used);
 
+// numpy Generator(PCG64).choice on the device (synth.cu).
+int synth_choice(const uint64_t *state, const uint64_t *inc, uint64_t offset, const double *cdf, const float *levels,
+                 int32_t k, int64_t count, float *out, cudaStream_t st);
+
 // Kernel-path overrides (cerdot_set_kernel_path); 0 = automatic.
 int kernel_path(int op);
 

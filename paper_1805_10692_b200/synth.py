@@ -120,33 +120,47 @@ def make_weights(cfg: LayerConfig, rng: np.random.Generator, rows: int | None = 
     return out
 
 
-def make_weights_device(cfg: LayerConfig, seed: int, device, row0: int = 0, rows: int | None = None,
-                        chunk_rows: int = 1024):
-    """Rows [row0, row0 + rows) of a config's W drawn ON THE DEVICE (torch), for the 32768^2 config whose
-    numpy draw takes a minute on the host.  Same codebook and pmf as ``make_weights`` (inverse-CDF sampling
-    of a uniform), but a different random stream, so it is statistically, not draw-for-draw, the numpy
-    layer.  Each block of ``chunk_rows`` global rows has its own generator seeded ``(seed, block)``, so a
-    row block is the same whichever shard draws it (row-sharded runs at any GPU count see one matrix)."""
+def _pcg64_words(rng: np.random.Generator):
+    st = rng.bit_generator.state
+    if st.get("bit_generator") != "PCG64":
+        raise ValueError("the device draw reproduces numpy's PCG64 generator only")
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    mask = (1 << 64) - 1
+    return (np.array([s & mask, s >> 64], dtype=np.uint64), np.array([inc & mask, inc >> 64], dtype=np.uint64))
+
+
+def make_weights_device(cfg: LayerConfig, seed: int, device, row0: int = 0, rows: int | None = None):
+    """Rows [row0, row0 + rows) of a config's W drawn ON THE DEVICE, bit-identical to ``make_weights`` with
+    ``np.random.default_rng(seed)`` (W is the first draw of the seeded generator): the
+    library's PCG64 kernel (cerdot_synth_choice) jumps to element row0 * n and reproduces numpy's
+    ``choice(K, p=pmf)``.  Used for the 32768^2 config, whose numpy draw takes about a minute on the host;
+    any row block is the same rows of the one seeded matrix, whichever shard draws it."""
     import torch
 
+    from . import _native
+
     m = cfg.m - row0 if rows is None else int(rows)
-    lv = torch.from_numpy(levels_of(cfg)).to(device)
-    cdf = torch.from_numpy(np.cumsum(pmf_of(cfg))).to(device)
-    cdf[-1] = 1.0
-    out = torch.empty((m, cfg.n), dtype=torch.float32, device=device)
-    g = torch.Generator(device=device)
-    r = row0
-    while r < row0 + m:
-        blk = r // chunk_rows
-        b0, b1 = blk * chunk_rows, min(cfg.m, (blk + 1) * chunk_rows)
-        g.manual_seed(seed * 1_000_003 + blk)
-        u = torch.rand((b1 - b0, cfg.n), generator=g, device=device, dtype=torch.float64)
-        lo, hi = max(r, b0), min(row0 + m, b1)
-        idx = torch.searchsorted(cdf, u[lo - b0:hi - b0], right=True).clamp_(max=cfg.k - 1)
-        out[lo - row0:hi - row0] = lv[idx]
-        del u, idx
-        r = hi
+    state, inc = _pcg64_words(np.random.default_rng(seed))
+    pmf = pmf_of(cfg)
+    cdf = pmf.cumsum()
+    cdf /= cdf[-1]
+    dev = torch.device(device)
+    cdf_d = torch.from_numpy(cdf).to(dev)
+    lv_d = torch.from_numpy(levels_of(cfg)).to(dev)
+    out = torch.empty((m, cfg.n), dtype=torch.float32, device=dev)
+    with torch.cuda.device(dev):
+        _native.check(_native.lib().cerdot_synth_choice(
+            state.ctypes.data, inc.ctypes.data, int(row0) * cfg.n, cdf_d.data_ptr(), lv_d.data_ptr(), cfg.k,
+            m * cfg.n, out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+        torch.cuda.current_stream(dev).synchronize()  # state / inc are host arrays read at launch
     return out
+
+
+def rng_after_weights(cfg: LayerConfig, seed: int) -> np.random.Generator:
+    """The seeded generator positioned after W's m * n draws (for the inputs, drawn next in §8(d)'s order)."""
+    rng = np.random.default_rng(seed)
+    rng.bit_generator.advance(cfg.m * cfg.n)
+    return rng
 
 
 def make_inputs(cfg: LayerConfig, rng: np.random.Generator, batch: int) -> np.ndarray:

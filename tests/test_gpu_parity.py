@@ -206,6 +206,22 @@ def test_long_rows_default_to_run_kernel_and_match_oracle():
         assert rel_err(cd.dot(enc, xr.astype(np.float32)), ref) <= REL_TOL, encode.__name__
 
 
+def test_device_draw_equals_numpy_draw():
+    """synth.make_weights_device (PCG64 on the device) is bit-identical to the seeded numpy draw, for whole
+    layers and for row blocks in the middle of config 5 (reached on the host with bit_generator.advance)."""
+    for name in ("oracle", "alexnet-fc6", "resnet-conv"):
+        cfg = synth.config(name)
+        host = synth.make_weights(cfg, np.random.default_rng(0))
+        assert np.array_equal(synth.make_weights_device(cfg, 0, "cuda").cpu().numpy(), host), name
+    cfg = synth.config("large")
+    for row0 in (0, 12345, 32700):
+        rng = np.random.default_rng(0)
+        rng.bit_generator.advance(row0 * cfg.n)
+        host = synth.make_weights(cfg, rng, rows=40)
+        dev = synth.make_weights_device(cfg, 0, "cuda", row0=row0, rows=40).cpu().numpy()
+        assert np.array_equal(dev, host), row0
+
+
 def test_large_config_properties():
     """Config 5 (32768^2, 256 levels) at full size: CER and CSER agree, scaling x by 2 is exact, and a
     row slice matches the oracle (size-independent checks; W drawn on the device)."""

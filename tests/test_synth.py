@@ -44,16 +44,47 @@ def test_survey_probe_nnz_config2():
     assert int(np.count_nonzero(w)) == 3395269
 
 
-def test_device_generator_row_blocks_and_pmf():
-    """make_weights_device: any row block equals the same rows of the full draw (row-sharded runs see
-    one matrix), and the level frequencies follow the pmf."""
-    torch = pytest.importorskip("torch")
-    cfg = synth.config("oracle")
-    full = synth.make_weights_device(cfg, 3, "cpu")
-    part = synth.make_weights_device(cfg, 3, "cpu", row0=200, rows=250)
-    assert torch.equal(full[200:450], part)
-    assert not torch.equal(full, synth.make_weights_device(cfg, 4, "cpu"))
-    vals, counts = np.unique(full.numpy(), return_counts=True)
-    freq = dict(zip(vals.tolist(), (counts / full.numel()).tolist()))
-    for v, p in zip(synth.levels_of(cfg).tolist(), synth.pmf_of(cfg)):
-        assert abs(freq.get(v, 0.0) - p) < 5 * np.sqrt(p * (1 - p) / full.numel()) + 1e-4
+M128 = (1 << 128) - 1
+PCG_MULT = 0x2360ED051FC65DA44385DF649FCCF645
+
+
+def _jump(state, inc, delta):
+    """The LCG jump-ahead csrc/synth.cu uses (PCG paper), restated with Python integers."""
+    acc_mult, acc_plus, cur_mult, cur_plus = 1, 0, PCG_MULT, inc
+    while delta:
+        if delta & 1:
+            acc_mult = acc_mult * cur_mult & M128
+            acc_plus = (acc_plus * cur_mult + cur_plus) & M128
+        cur_plus = (cur_mult + 1) * cur_plus & M128
+        cur_mult = cur_mult * cur_mult & M128
+        delta >>= 1
+    return (acc_mult * state + acc_plus) & M128
+
+
+def _xsl_rr(state):
+    x = (state >> 64) ^ (state & ((1 << 64) - 1))
+    rot = state >> 122
+    return ((x >> rot) | (x << (64 - rot))) & ((1 << 64) - 1)
+
+
+def test_pcg64_restatement_matches_numpy():
+    """The device generator's algorithm (csrc/synth.cu): element i of numpy's choice(K, p) is
+    searchsorted(cdf, (xsl_rr(jump(s0, i + 1)) >> 11) * 2^-53, 'right'), including lane-strided jumps of 32."""
+    cfg = synth.config("large")
+    rng = np.random.default_rng(7)
+    st = rng.bit_generator.state["state"]
+    s0, inc = st["state"], st["inc"]
+    draw = rng.choice(cfg.k, size=200, p=synth.pmf_of(cfg))
+    cdf = synth.pmf_of(cfg).cumsum()
+    cdf /= cdf[-1]
+    for lane in (0, 5, 31):
+        s = _jump(s0, inc, lane + 1)
+        for e in range(lane, 200, 32):
+            u = (_xsl_rr(s) >> 11) * (1.0 / 9007199254740992.0)
+            assert int(np.searchsorted(cdf, u, side="right")) == draw[e]
+            s = _jump(s, inc, 32)
+    # the inputs follow W in the draw order: the generator advanced past m*n draws
+    a = synth.rng_after_weights(synth.config("oracle"), 3).standard_normal(5)
+    r = np.random.default_rng(3)
+    synth.make_weights(synth.config("oracle"), r)
+    assert np.array_equal(a, r.standard_normal(5))

@@ -3,7 +3,8 @@ every variant against the first one.  All mat-mat kernels compute each column in
 their outputs must be identical.
 
 Usage: python tools/mm_time.py [config:batch ...]
-Variants: MM_VARIANTS="0 1 ..." sets CERDOT_MM_PATH per variant ("auto" = unset).
+Variants: MM_VARIANTS="1 2 3 ..." pins the mat-mat kernel (cerdot_set_kernel_path: 1 flat, 2 per-segment,
+3 tiled, 4 tiled sum-then-multiply; "auto" = 0).
 """
 import json
 import os
@@ -19,10 +20,9 @@ from paper_1805_10692_b200 import synth  # noqa: E402
 
 
 def set_variant(v: str):
-    if v == "auto":
-        os.environ.pop("CERDOT_MM_PATH", None)
-    else:
-        os.environ["CERDOT_MM_PATH"] = v
+    from paper_1805_10692_b200._native import lib
+
+    lib().cerdot_set_kernel_path(1, 0 if v == "auto" else int(v))  # CERDOT_PATH_MATMAT
 
 
 def graph_us(encs, xs, ys, reps=5):

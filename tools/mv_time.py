@@ -1,8 +1,8 @@
 """Graph-replayed cold mat-vec time (us per call) for each config x kind; prints one JSON line per case.
 
 Usage: python tools/mv_time.py [config ...]   (CERDOT_LIB selects the library for A/B runs)
-MV_VARIANTS="1 3" times each CERDOT_MATVEC_PATH value in one process ("auto" = unset) and reports each
-variant's max|y - y_first| / max|y_first| against the first.
+MV_VARIANTS="1 3" times each mat-vec kernel path (cerdot_set_kernel_path: 1 window, 2 tile, 3 run; "auto")
+in one process and reports each variant's max|y - y_first| / max|y_first| against the first.
 """
 import json
 import os
@@ -15,6 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_1805_10692_b200 as cd  # noqa: E402
 from paper_1805_10692_b200 import synth  # noqa: E402
+from paper_1805_10692_b200._native import force_path  # noqa: E402
 
 
 def graph_us(encs, xs, ys, reps=20):
@@ -55,12 +56,9 @@ def main():
             xs = [torch.from_numpy(x).cuda().reshape(-1) for _ in range(R)]
             ref = None
             for var in os.environ.get("MV_VARIANTS", "auto").split():
-                if var == "auto":
-                    os.environ.pop("CERDOT_MATVEC_PATH", None)
-                else:
-                    os.environ["CERDOT_MATVEC_PATH"] = var
                 ys = [torch.full((cfg.m,), float("nan"), device="cuda") for _ in range(R)]
-                us = graph_us(copies, xs, ys)
+                with force_path("matvec", 0 if var == "auto" else int(var)):
+                    us = graph_us(copies, xs, ys)
                 y = ys[0].double().cpu().numpy()
                 if ref is None:
                     ref = y

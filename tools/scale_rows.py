@@ -2,12 +2,13 @@ import sys, os, json, numpy as np, torch
 sys.path.insert(0, os.getcwd())
 import paper_1805_10692_b200 as cd
 from paper_1805_10692_b200 import synth, shard
+from paper_1805_10692_b200._native import lib
 cfg = synth.config("alexnet-fc6")
 w, xs = synth.make_layer(cfg)
 enc = cd.encode_cer(torch.from_numpy(w).cuda())
 x = torch.from_numpy(xs[1]).cuda()
 for path in ("1", "2"):
-    os.environ["CERDOT_MATVEC_PATH"] = path
+    lib().cerdot_set_kernel_path(0, int(path))  # CERDOT_PATH_MATVEC
     for rows in (512, 1024, 2048, 4096):
         e = shard.slice_rows(enc, 0, rows) if rows < 4096 else enc
         y = torch.empty(rows, device="cuda")

@@ -1,4 +1,4 @@
-"""Print per-CTA phase timestamps of the window mat-vec (CERDOT_TRACE=1), relative to the earliest start.
+"""Print per-CTA phase timestamps of the window mat-vec (CERDOT_PATH_TRACE), relative to the earliest start.
 
 Usage: python tools/trace_matvec.py [config:rows:kind ...]   (default alexnet-fc6:4096:cer/cser)
 Needs a library built with -DCERDOT_TRACE_KERNELS (NVCC_EXTRA=-DCERDOT_TRACE_KERNELS python -m paper_1805_10692_b200.build --force).
@@ -16,12 +16,16 @@ e = shard.slice_rows(enc, 0, rows) if rows < cfg.m else enc
 x = torch.from_numpy(xs[1]).cuda(); y = torch.empty(rows, device="cuda")
 for _ in range(3): cd.dot_device(e, x, out=y)
 torch.cuda.synchronize()
-os.environ["CERDOT_TRACE"] = "1"
+from paper_1805_10692_b200._native import lib
+lib().cerdot_set_kernel_path(0, 1)  # CERDOT_PATH_MATVEC: the window kernel
+for _ in range(3): cd.dot_device(e, x, out=y)
+torch.cuda.synchronize()
+lib().cerdot_set_kernel_path(4, 1)  # CERDOT_PATH_TRACE
 cd.dot_device(e, x, out=y); torch.cuda.synchronize()
 '''
 cases = [tuple(a.split(":")) for a in sys.argv[1:]] or [("alexnet-fc6", "4096", "cer"), ("alexnet-fc6", "4096", "cser")]
 for cfgname, rows, kind in cases:
-    env = dict(os.environ, CERDOT_MATVEC_PATH="1")
+    env = dict(os.environ)
     out = subprocess.run([sys.executable, "-c", code, cfgname, str(rows), kind], capture_output=True, text=True,
                          env=env).stdout
     recs = [list(map(int, re.findall(r"(\d+)", l)[:12])) for l in out.splitlines() if l.startswith("TRACE")]
