@@ -3,23 +3,24 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config NAME] [--cases all|none]
 
-Headline workload (``config.workload``): BASELINE configs[1], the
-AlexNet-fc6-shaped layer (W 4096x9216, 128 levels, 91% zeros), one step =
-one CER mat-vec + one CSER mat-vec (B=1) of one input vector.  Inputs are
-resident in HBM; 16 rotating encoded copies (> 2x the 126 MB L2) keep every
-step cold.  N>1 (torchrun): weak scaling — each rank owns one such row block
-(seed + rank), x is replicated and the y blocks are all-gathered over NCCL.
+Workload (``config.workload``), one step = one CER mat-vec + one CSER mat-vec (B=1) of one input vector:
+* N = 1 (default ``--config auto``): BASELINE configs[1], the AlexNet-fc6-shaped layer (W 4096x9216,
+  128 levels, 91% zeros).  Inputs resident in HBM; 16 rotating encoded copies (> 2x the 126 MB L2)
+  keep every step cold.
+* N > 1 (torchrun, default ``--config auto``): BASELINE configs[4], the 32768^2 layer (256 levels, 70%
+  zeros) row-sharded over the ranks (strong scaling).  Every rank draws the one seeded matrix on its GPU
+  and encodes it; its shard is a row slice of that GLOBAL encoding (SURVEY.md §8(e)), cut on the device;
+  x is replicated and y is assembled by the fused NVLink peer-store exchange (NCCL all-gather fallback).
+  ``--config large`` gives the same workload at N = 1 (the scaling series' first point).
 
-JSON line (rank 0): metric/value/unit (achieved GB/s of algorithmic bytes:
-reference storage_bits/8 of CER+CSER + x + y per step), ms_per_step,
-roofline (mat-vec kernel vs measured HBM copy peak), gmacs (dense-equivalent),
-e2e (public numpy API with host x, H2D + D2H inside the timed region),
-cpu_baseline (the oracle port of the reference's numpy path on this host),
-clocks (NVML during the timed region), gpu_launches, and ``cases``: the other
-BASELINE configs/batches (B=64, 128, 1568) measured the same way.
+JSON line (rank 0): metric/value/unit (achieved GB/s of algorithmic bytes: reference storage_bits/8 of
+CER+CSER + x + y per step), ms_per_step, roofline (mat-vec kernels vs measured HBM copy peak), gmacs
+(dense-equivalent), e2e (public numpy API with host x, H2D + D2H inside the timed region), cpu_baseline
+(the oracle port of the reference's numpy path on this host), clocks (NVML during the timed region),
+gpu_launches, and ``cases``: the other BASELINE configs/batches measured the same way.
 
-``--impl reference``: the reference's CPU algorithm (oracle numpy port, all
-host threads) on the same workload and metric; rank 0 only.
+``--impl reference``: the reference's CPU algorithm (oracle numpy port, all host threads) on the same
+workload, metric and ``config``; rank 0 only.
 """
 
 from __future__ import annotations
@@ -186,10 +187,36 @@ def cpu_baseline_sample(w: np.ndarray, x: np.ndarray, repeats: int = 5, threads:
 
 
 def port_bytes(enc: dict, batch: int) -> int:
-    bits = len(enc["omega"]) * 32 + enc["colI"].nbytes * 8 + enc["omegaPtr"].nbytes * 8 + enc["rowPtr"].nbytes * 8
+    """Algorithmic bytes of an oracle-port encoding at the REFERENCE's widths (storage_bits/8, formats.py:
+    454-479: each index array at the auto width of its largest value -- a row block's arrays are int64 views)
+    + x + y: the same count as the GPU arm's alg_bytes for the same rows."""
+    from oracle import numpy_port
+
+    w = numpy_port.width_for
+    s = len(enc["omegaPtr"]) - 1
+    nnz = len(enc["colI"])
+    k = len(enc["omega"])
+    bits = k * 32 + nnz * w(max(enc["n"] - 1, 0)) + (s + 1) * w(nnz) + (enc["m"] + 1) * w(s)
     if enc["kind"] == "cser":
-        bits += enc["omegaI"].nbytes * 8
+        bits += s * w(max(k - 1, 0))
     return bits // 8 + enc["n"] * batch * 4 + enc["m"] * batch * 4
+
+
+def resolve_config(name: str, world: int) -> str:
+    """``auto``: the AlexNet fc6 layer on one GPU; the 32768^2 layer row-sharded over N > 1 GPUs."""
+    if name != "auto":
+        return name
+    return "large" if world > 1 else "alexnet-fc6"
+
+
+def workload_config(cfg, world: int, seed: int) -> dict:
+    """The ``config`` object of the JSON line: the workload only, identical in both arms."""
+    strong = cfg.name == "large"
+    rows = f"one matrix row-sharded over {world} rank(s)" if strong else f"one {cfg.m}-row layer per rank ({world})"
+    return {"workload": f"{cfg.name} {cfg.m}x{cfg.n} K={cfg.k} p0={cfg.p_zero}: CER + CSER mat-vec (B=1) per step, "
+                        f"{rows}", "seed": seed, "batch": 1, "n_ranks": world,
+            "parallelism": f"rows x{world}" if world > 1 else "single GPU",
+            "scaling": "strong" if strong else "weak"}
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -201,20 +228,22 @@ def run_reference(args):
         return 0
     from paper_1805_10692_b200 import synth
 
-    cfg = synth.config(args.config)
-    w, xs = synth.make_layer(cfg, seed=args.seed)
+    cfg = synth.config(resolve_config(args.config, world))
     threads = os.cpu_count() or 1
     from oracle import numpy_port
 
+    x = synth.input_for(cfg, args.seed, 1).astype(np.float64)
+    strong = cfg.name == "large"
+    # the reference path on a bounded row sample of the workload (the full 32768^2 draw takes a host minute)
+    probe_rows = min(cfg.m, 512 if strong else cfg.m)
+    w = synth.make_weights(cfg, np.random.default_rng(args.seed), rows=probe_rows)
     full = [numpy_port.encode_cer(w), numpy_port.encode_cser(w)]
-    x = xs[1].astype(np.float64)
-    # size each step to a bounded row sample so the K-step run ends within ~budget seconds
     t0 = time.perf_counter()
     for e in full:
         numpy_port.dot_threaded(e, x, threads)
-    t_full = time.perf_counter() - t0
+    t_probe = time.perf_counter() - t0
     budget = args.ref_budget_s / max(1, args.steps + args.warmup)
-    rows = int(min(cfg.m, max(threads, cfg.m * budget / max(t_full, 1e-9))))
+    rows = int(min(probe_rows, max(threads, probe_rows * budget / max(t_probe, 1e-9))))
     encs = [numpy_port.row_block(e, 0, rows) for e in full]
     step_bytes = sum(port_bytes(e, 1) for e in encs)
     for _ in range(max(args.warmup, 1)):
@@ -229,13 +258,13 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "cer_cser_dot_achieved_gbs", "value": round(value, 4), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} {cfg.m}x{cfg.n} CER+CSER mat-vec (B=1)", "seed": args.seed},
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(cfg, world, args.seed),
         "gmacs": round(2 * rows * cfg.n / dt / 1e9, 4),
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": "oracle/numpy_port (the reference lemt numpy algorithm, bitwise-pinned): "
-                                   f"CER+CSER mat-vec on rows [0,{rows}) of the {cfg.m}-row layer per step "
-                                   f"(full-layer step {t_full * 1e3:.1f} ms), split over {threads} threads"},
+                                   f"CER+CSER mat-vec on rows [0,{rows}) of the {cfg.m}-row layer per step, "
+                                   f"split over {threads} threads; bytes at the reference's index widths"},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -296,12 +325,9 @@ def measure_case(cd, torch, cfg_name: str, batch: int, steps: int, warmup: int, 
     from paper_1805_10692_b200 import synth
 
     cfg = synth.config(cfg_name)
-    rng = np.random.default_rng(seed)
-    if cfg.m * cfg.n > 10**9:  # config 5: the numpy draw takes a minute on the host; draw W on the device
-        wt = synth.make_weights_device(cfg, seed, device)
-    else:
-        wt = torch.from_numpy(synth.make_weights(cfg, rng)).to(device)
-    x = synth.make_inputs(cfg, rng, batch)
+    # W: the seeded numpy draw (for config 5 reproduced on the device, bit-identical); X: drawn after W
+    wt = synth.make_weights_device(cfg, seed, device)
+    x = synth.input_for(cfg, seed, batch)
     out = {"config": cfg_name, "m": cfg.m, "n": cfg.n, "batch": batch}
     peak, _ = _peaks()
     for kind, encode in (("cer", cd.encode_cer), ("cser", cd.encode_cser)):
@@ -413,27 +439,24 @@ def run_ours(args):
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     import paper_1805_10692_b200 as cd
-    from paper_1805_10692_b200 import synth
+    from paper_1805_10692_b200 import shard, synth
     from paper_1805_10692_b200.shard import RowShardedDot
 
-    cfg = synth.config(args.config)
+    cfg = synth.config(resolve_config(args.config, world))
     peak, peak_src = _peaks()
-    strong = cfg.m * cfg.n > 10**9
+    strong = cfg.name == "large"
+    x_host = synth.input_for(cfg, args.seed, 1)
     if strong:
-        # config 5: ONE matrix row-sharded over the ranks (strong scaling); every rank draws only its
-        # row block on the device (synth.make_weights_device: a block is the same at any GPU count)
-        bounds = [cfg.m * r // world for r in range(world + 1)]
-        wt = synth.make_weights_device(cfg, args.seed, device, row0=bounds[rank], rows=bounds[rank + 1] - bounds[rank])
-        x_host = synth.make_inputs(cfg, np.random.default_rng(args.seed + 1), 1)
-        w = wt[: min(256, wt.shape[0])].cpu().numpy()  # CPU baseline sample (rows of the block)
-        rows = [bounds[r + 1] - bounds[r] for r in range(world)]
+        # config 5: ONE seeded matrix, encoded once (every rank computes the same global encoding from the
+        # same device draw); a rank's shard is a row slice of that global encoding, cut on the device
+        wt = synth.make_weights_device(cfg, args.seed, device)
+        w = wt[:256].cpu().numpy()  # CPU baseline sample (rows [0, 256))
     else:
         # ---- this rank's row block (weak scaling: seed + rank)
-        w, xs = synth.make_layer(cfg, seed=args.seed + rank)
-        x_host = xs[1] if 1 in xs else synth.make_inputs(cfg, np.random.default_rng(args.seed + 1), 1)
+        w = synth.make_weights(cfg, np.random.default_rng(args.seed + rank))
+        if rank:
+            x_host = synth.input_for(cfg, args.seed, 1)  # x is replicated: every rank uses seed's x
         wt = torch.from_numpy(w).to(device)
-        rows = [cfg.m] * world
-    m_local = int(wt.shape[0])
     cd.encode_cer(wt), cd.encode_cser(wt)  # warm the conversion kernels (first-launch setup)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -444,17 +467,31 @@ def run_ours(args):
     cser = cd.encode_cser(wt)
     torch.cuda.synchronize()
     t_enc_cser = time.perf_counter() - t0
+    dense_rows = int(wt.shape[0])
+    del wt
+    torch.cuda.empty_cache()
+    if strong:
+        total_bytes = alg_bytes(cer, 1) + alg_bytes(cser, 1)  # the whole matrix per step
+        bounds = shard.plan_rows(cer, world) if world > 1 else [0, cfg.m]
+        rows = [bounds[r + 1] - bounds[r] for r in range(world)]
+        if world > 1:
+            cer = shard.slice_rows_device(cer, bounds[rank], bounds[rank + 1])
+            cser = shard.slice_rows_device(cser, bounds[rank], bounds[rank + 1])
+            torch.cuda.empty_cache()
+    else:
+        rows = [cfg.m] * world
+        total_bytes = None
+    m_local = cer.m
     step_bytes = alg_bytes(cer, 1) + alg_bytes(cser, 1)
+    if total_bytes is None:
+        total_bytes = world * step_bytes
     per_copy = cer.device_encoding().format_bytes + cser.device_encoding().format_bytes + 2 * x_host.nbytes
     rotate = max(ROTATE_MIN if per_copy < L2_BYTES else 2, -(-2 * L2_BYTES // per_copy))
-    cers = [_clone(cd, cer) for _ in range(rotate)]
-    csers = [_clone(cd, cser) for _ in range(rotate)]
+    cers = [cer] + [_clone(cd, cer) for _ in range(rotate - 1)]
+    csers = [cser] + [_clone(cd, cser) for _ in range(rotate - 1)]
     xdev = [torch.from_numpy(x_host).to(device) for _ in range(rotate)]
     ycer = [torch.empty(m_local, dtype=torch.float32, device=device) for _ in range(rotate)]
     ycser = [torch.empty(m_local, dtype=torch.float32, device=device) for _ in range(rotate)]
-    if strong:
-        del wt
-        torch.cuda.empty_cache()
 
     sampler = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     if world == 1:
@@ -515,17 +552,6 @@ def run_ours(args):
         secs = start.elapsed_time(end) / 1e3
     secs = max_over_ranks(secs, world, device)
     t_step = secs / args.steps
-    if strong:  # bytes of the whole matrix (every rank's block) per step
-        if world > 1:
-            import torch.distributed as dist
-
-            tb = torch.tensor([step_bytes], dtype=torch.int64, device=device)
-            dist.all_reduce(tb)
-            total_bytes = int(tb.item())
-        else:
-            total_bytes = step_bytes
-    else:
-        total_bytes = world * step_bytes
     value = total_bytes / t_step / 1e9
 
     # ---- e2e through the public numpy API (H2D of x, D2H of y inside the region)
@@ -560,7 +586,7 @@ def run_ours(args):
         cpu_t, port_encs = cpu_baseline_sample(w, x_host, repeats=args.cpu_repeats)
         cpu_bytes = sum(port_bytes(e, 1) for e in port_encs)
         if not strong:
-            assert cpu_bytes == step_bytes, (cpu_bytes, step_bytes)
+            assert cpu_bytes == step_bytes, (cpu_bytes, step_bytes)  # the same bytes in both arms
         cases = []
         if args.cases == "all" and world == 1:
             plan = [("alexnet-fc6", 64), ("vgg-fc6", 1), ("vgg-fc6", 128), ("resnet-conv", 1),
@@ -570,7 +596,7 @@ def run_ours(args):
                 if name == "large":
                     steps_c = 20 if b == 1 else 3
                 cases.append(measure_case(cd, torch, name, b, steps_c, 3, args.seed, device))
-        libs = (library_baseline_times(torch, wt, x_host, device)
+        libs = (library_baseline_times(torch, torch.from_numpy(w).to(device), x_host, device)
                 if (args.cases == "all" and world == 1 and not strong) else {})
         fmt_b = {"cer": cd.storage_bits(cer) // 8, "cser": cd.storage_bits(cser) // 8}
         traffic = _ncu_traffic(cfg.name)
@@ -586,17 +612,17 @@ def run_ours(args):
             "scaling": "strong" if strong else "weak",
             "vs_baseline": None,
             "dtype": "f32",
-            "data": ("synthetic (config 5, drawn on the device per row block; SURVEY.md §8(d))" if strong else
+            "data": ("synthetic: the seeded numpy draw of SURVEY.md §8(d) (config 5 reproduced bit-identically on "
+                     "the device by synth.cu's PCG64 kernel), x drawn after W" if strong else
                      "synthetic (seeded stand-in for the pretrained AlexNet fc6 layer; SURVEY.md §8(d))"),
-            "config": {
-                "workload": f"{cfg.name} {cfg.m}x{cfg.n} K={cfg.k} p0={cfg.p_zero}: CER + CSER mat-vec (B=1) per "
-                            f"step, {world} row block(s) of {m_local} rows"
-                            + (" (one matrix row-sharded over the ranks)" if strong else " (one block per rank)"),
+            "config": workload_config(cfg, world, args.seed),
+            "run": {
                 "l2": f"inputs larger than L2: {rotate} rotating encoded copies "
                       f"({rotate * per_copy / 2**20:.0f} MiB > 126 MiB L2)",
-                "alg_bytes_per_step": step_bytes,
+                "alg_bytes_per_step": total_bytes,
+                "rank0_alg_bytes_per_step": step_bytes,
+                "rows_per_rank": rows,
                 "format_bytes": fmt_b,
-                "parallelism": f"rows x{world} (all-gather of y)" if world > 1 else "single GPU",
                 "exchange": exchange if world > 1 else None,
                 "timing": "CUDA graphs of rotating steps, CUDA events around exactly K steps" if world == 1
                           else "eager, CUDA events, max over ranks",
@@ -626,7 +652,7 @@ def run_ours(args):
                                        f"{args.cpu_repeats}, single thread (as the reference)",
                              "host_cores": os.cpu_count()},
             "conversion": {"cer_s": round(t_enc_cer, 5), "cser_s": round(t_enc_cser, 5),
-                           "dense_input_gbs": round(m_local * cfg.n * 4 / t_enc_cer / 1e9, 2)},
+                           "dense_input_gbs": round(dense_rows * cfg.n * 4 / t_enc_cer / 1e9, 2)},
             "clocks": clocks,
             "gpu_launches": 2 * args.steps,
             "library_baselines": libs,
@@ -666,7 +692,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=4000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", default="alexnet-fc6")
+    ap.add_argument("--config", default="auto", help="auto: alexnet-fc6 at N=1, large (config 5) at N>1")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cases", choices=("all", "none"), default="all")
     ap.add_argument("--case-budget-s", type=float, default=0.05)

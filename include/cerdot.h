@@ -277,9 +277,10 @@ int cerdot_synth_choice(const uint64_t *state, const uint64_t *inc, uint64_t off
 /* Row-shard planner (host).  row_ptr / omega_ptr are HOST arrays of the
  * given widths.  Writes parts+1 row bounds (bounds[0]=0, bounds[parts]=m)
  * splitting rows into contiguous blocks of near-equal encoded bytes
- * (entries*col_bytes + segments*ptr_bytes + rows*row_bytes). */
+ * (entries*col_bytes + segments*(ptr_bytes + omegaI bytes) + rows*row_bytes);
+ * omega_index_bits = 0 for CER. */
 int cerdot_shard_plan(const void *row_ptr, int32_t row_ptr_bits, const void *omega_ptr, int32_t omega_ptr_bits,
-                      int32_t col_bits, int64_t m, int32_t parts, int64_t *bounds);
+                      int32_t col_bits, int32_t omega_index_bits, int64_t m, int32_t parts, int64_t *bounds);
 
 #ifdef __cplusplus
 }

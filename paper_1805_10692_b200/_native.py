@@ -101,7 +101,7 @@ _SIGNATURES = {
     "cerdot_dot_host_workspace_bytes": (_SZ, [ctypes.POINTER(CerdotMatrix), _I64]),
     "cerdot_dot_host": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _I64, _I64, _P, _I64, _P, _SZ, _P]),
     "cerdot_row_entries": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _P, _P]),
-    "cerdot_shard_plan": (ctypes.c_int, [_P, _I32, _P, _I32, _I32, _I64, _I32, ctypes.POINTER(ctypes.c_int64)]),
+    "cerdot_shard_plan": (ctypes.c_int, [_P, _I32, _P, _I32, _I32, _I32, _I64, _I32, ctypes.POINTER(ctypes.c_int64)]),
     "cerdot_tile_view_rows": (_I32, [ctypes.POINTER(CerdotMatrix), _I64]),
     "cerdot_tile_view_workspace_bytes": (_SZ, [ctypes.POINTER(CerdotMatrix), _I32]),
     "cerdot_tile_view_build": (ctypes.c_int, [ctypes.POINTER(CerdotMatrix), _I32, _P, _P, _P, _SZ, _P]),

@@ -289,20 +289,21 @@ int cerdot_tile_view_build(const cerdot_matrix *a, int32_t tile_rows, uint32_t *
 }
 
 int cerdot_shard_plan(const void *row_ptr, int32_t row_ptr_bits, const void *omega_ptr, int32_t omega_ptr_bits,
-                      int32_t col_bits, int64_t m, int32_t parts, int64_t *bounds) {
+                      int32_t col_bits, int32_t omega_index_bits, int64_t m, int32_t parts, int64_t *bounds) {
   if (parts < 1) return fail(CERDOT_E_VALUE, "parts must be >= 1");
   if (m < 0 || bounds == nullptr || (m > 0 && (row_ptr == nullptr || omega_ptr == nullptr)))
     return fail(CERDOT_E_VALUE, "invalid shard-plan arguments");
-  if (!valid_bits(row_ptr_bits) || !valid_bits(omega_ptr_bits) || !valid_bits(col_bits))
+  if (!valid_bits(row_ptr_bits) || !valid_bits(omega_ptr_bits) || !valid_bits(col_bits) ||
+      (omega_index_bits != 0 && !valid_bits(omega_index_bits)))
     return fail(CERDOT_E_VALUE, "index bits must be one of (8, 16, 32)");
-  // prefix of encoded bytes per row: entries*col + segments*ptr + row pointer
+  // prefix of encoded bytes per row: entries*col + segments*(ptr + CSER omegaI) + row pointer
+  const double seg_bytes = (omega_ptr_bits + omega_index_bits) / 8.0;
   std::vector<double> prefix(static_cast<size_t>(m) + 1, 0.0);
   for (int64_t r = 0; r < m; ++r) {
     const uint64_t s0 = host_index(row_ptr, row_ptr_bits, r), s1 = host_index(row_ptr, row_ptr_bits, r + 1);
     const uint64_t e0 = host_index(omega_ptr, omega_ptr_bits, static_cast<int64_t>(s0));
     const uint64_t e1 = host_index(omega_ptr, omega_ptr_bits, static_cast<int64_t>(s1));
-    prefix[r + 1] = prefix[r] + (e1 - e0) * (col_bits / 8.0) + (s1 - s0) * (omega_ptr_bits / 8.0) +
-                    row_ptr_bits / 8.0;
+    prefix[r + 1] = prefix[r] + (e1 - e0) * (col_bits / 8.0) + (s1 - s0) * seg_bytes + row_ptr_bits / 8.0;
   }
   bounds[0] = 0;
   for (int p = 1; p < parts; ++p) {

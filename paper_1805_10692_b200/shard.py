@@ -37,9 +37,10 @@ def plan_rows(enc, parts: int) -> list[int]:
     rp = np.ascontiguousarray(enc.row_ptr)
     op = np.ascontiguousarray(enc.omega_ptr)
     bounds = (ctypes.c_int64 * (parts + 1))()
+    oi_bits = enc.omega_index_bits if isinstance(enc, CserMatrix) else 0
     _native.check(_native.lib().cerdot_shard_plan(rp.ctypes.data, rp.dtype.itemsize * 8, op.ctypes.data,
-                                                  op.dtype.itemsize * 8, enc.col_index_bits, enc.m, parts,
-                                                  bounds))
+                                                  op.dtype.itemsize * 8, enc.col_index_bits, oi_bits, enc.m,
+                                                  parts, bounds))
     return list(bounds)
 
 
@@ -62,6 +63,56 @@ def slice_rows(enc, r0: int, r1: int):
         return CserMatrix(enc.omega, col, enc.omega_index[s0:s1], omega_ptr, row_ptr, r1 - r0, enc.n,
                           enc.element_bits, enc.mode_index)
     return CerMatrix(enc.omega, col, omega_ptr, row_ptr, r1 - r0, enc.n, enc.element_bits)
+
+
+def slice_rows_device(enc, r0: int, r1: int):
+    """Rows [r0, r1) of a DEVICE-resident encoding as a new device-resident encoding, cut on the device
+    (no host round trip of the index arrays): the same slice as ``slice_rows`` -- rowPtr / omegaPtr
+    rebased, the colI (and CSER omegaI) spans copied, omega unchanged, the global widths kept -- plus the
+    derived rowEntry index of the block."""
+    import torch
+
+    from .device import DeviceEncoding, torch_mod  # noqa: F401
+
+    dev = enc.device_encoding()
+    if not 0 <= r0 <= r1 <= dev.m:
+        raise ValueError(f"row block [{r0}, {r1}) out of range for m={dev.m}")
+    tdt = {8: torch.uint8, 16: torch.uint16, 32: torch.uint32}
+
+    def view(name, start, stop):
+        b = dev.bits[name] // 8
+        o = dev.offsets[name]
+        return dev.arena[o + start * b: o + stop * b].view(tdt[dev.bits[name]])
+
+    rp = view("rowPtr", r0, r1 + 1).to(torch.int64)
+    s0, s1 = int(rp[0]), int(rp[-1])
+    op = view("omegaPtr", s0, s1 + 1).to(torch.int64)
+    e0, e1 = int(op[0]), int(op[-1])
+    m, segs, nnz = r1 - r0, s1 - s0, e1 - e0
+    offsets, total = DeviceEncoding.layout(dev.kind, m, dev.k, nnz, segs, dev.bits)
+    arena = torch.zeros(total, dtype=torch.uint8, device=dev.device)
+
+    def put(name, t):
+        o = offsets[name]
+        raw = t.contiguous().view(torch.uint8)
+        arena[o: o + raw.numel()] = raw
+
+    put("omega", dev.arena[dev.offsets["omega"]: dev.offsets["omega"] + 8 * dev.k])
+    put("colI", view("colI", e0, e1))
+    put("omegaPtr", (op - e0).to(tdt[dev.bits["omegaPtr"]]))
+    put("rowPtr", (rp - s0).to(tdt[dev.bits["rowPtr"]]))
+    if dev.kind == _native.CSER:
+        put("omegaI", view("omegaI", s0, s1))
+    seg_rows = rp[1:] - rp[:-1]
+    nnz_rows = op[(rp[1:] - s0)] - op[(rp[:-1] - s0)] if m else seg_rows
+    new = DeviceEncoding(dev.kind, m, dev.n, dev.k, nnz, segs, dev.mode_index, dev.background, dict(dev.bits), arena,
+                         offsets, int(nnz_rows.max()) if m else 0, int(seg_rows.max()) if m else 0)
+    with torch.cuda.device(dev.device):
+        new.fill_row_entries(torch.cuda.current_stream(dev.device).cuda_stream)
+    cls = type(enc)
+    if isinstance(enc, CserMatrix):
+        return cls(None, None, None, None, None, m, enc.n, enc.element_bits, enc.mode_index, _device=new)
+    return cls(None, None, None, None, m, enc.n, enc.element_bits, _device=new)
 
 
 class RowShardedDot:

@@ -171,6 +171,22 @@ def make_inputs(cfg: LayerConfig, rng: np.random.Generator, batch: int) -> np.nd
     return np.ascontiguousarray(x[:, 0]) if batch == 1 else x
 
 
+def input_for(cfg: LayerConfig, seed: int, batch: int) -> np.ndarray:
+    """X of a listed batch in §8(d)'s order (drawn after W, batches in the listed order); B=1 when the
+    config does not list it: column 0 of the first listed batch's draw."""
+    rng = rng_after_weights(cfg, seed)
+    first = None
+    for b in cfg.batches:
+        x = make_inputs(cfg, rng, b)
+        if b == batch:
+            return x
+        if first is None:
+            first = x
+    if batch == 1:
+        return np.ascontiguousarray(first[:, 0])
+    raise ValueError(f"batch {batch} is not listed for config {cfg.name} ({cfg.batches})")
+
+
 def make_layer(cfg: LayerConfig | str, seed: int = 0, rows: int | None = None):
     """(W, {B: X}) for a config, drawn in the documented order."""
     if not isinstance(cfg, LayerConfig):

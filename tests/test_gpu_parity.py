@@ -606,3 +606,26 @@ def test_randomized_round_trip_and_dot():
             assert np.array_equal(cd.decode(enc).values, w), (trial, kind)
             assert np.array_equal(cd.dot(enc, x), w @ x), (trial, kind)
             assert np.array_equal(cd.dot(enc, x[:, 0]), w @ x[:, 0]), (trial, kind)
+
+
+def test_device_row_slices_equal_host_slices():
+    """shard.slice_rows_device (bench.py's N>1 shards of the global encoding) == shard.slice_rows, array by
+    array, and the blocks' products concatenate to the full product within the bar (not bitwise: a block's
+    kernel choice and window alignment follow its own row count and rebased entry offsets)."""
+    from paper_1805_10692_b200 import shard
+
+    w, xs = synth.make_layer("alexnet-fc6")
+    x = torch.from_numpy(xs[1]).cuda()
+    for encode in (cd.encode_cer, cd.encode_cser):
+        full = encode(torch.from_numpy(w).cuda())
+        y_full = cd.dot(full, x)
+        for parts in (2, 4, 8):
+            bounds = shard.plan_rows(full, parts)
+            ys = []
+            for a, b in zip(bounds[:-1], bounds[1:]):
+                d, h = shard.slice_rows_device(full, a, b), shard.slice_rows(full, a, b)
+                for f in ("col_index", "omega_ptr", "row_ptr") + (("omega_index",) if encode is cd.encode_cser else ()):
+                    assert np.array_equal(getattr(d, f), getattr(h, f)), (f, a, b)
+                ys.append(cd.dot(d, x))
+            assert rel_err(torch.cat(ys).cpu().numpy(), y_full.double().cpu().numpy()) <= REL_TOL, (encode.__name__,
+                                                                                                    parts)

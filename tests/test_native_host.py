@@ -52,19 +52,19 @@ def test_shard_plan_balances_bytes():
     row_ptr = np.concatenate(([0], np.cumsum(segs))).astype(np.uint32)
     sizes = rng.integers(0, 50, size=int(row_ptr[-1]))
     omega_ptr = np.concatenate(([0], np.cumsum(sizes))).astype(np.uint32)
-    for parts in (1, 2, 3, 8):
-        b = (ctypes.c_int64 * (parts + 1))()
-        assert L.cerdot_shard_plan(row_ptr.ctypes.data, 32, omega_ptr.ctypes.data, 32, 16, m, parts, b) == 0
-        bounds = list(b)
-        assert bounds[0] == 0 and bounds[-1] == m and all(x <= y for x, y in zip(bounds, bounds[1:]))
-        row_bytes = 2 * np.diff(omega_ptr.astype(np.int64))[...]
-        per_row = np.array([2 * (omega_ptr[row_ptr[r + 1]] - omega_ptr[row_ptr[r]]) + 4 * segs[r] + 4
-                            for r in range(m)], dtype=float)
-        del row_bytes
-        shares = [per_row[a:c].sum() for a, c in zip(bounds[:-1], bounds[1:])]
-        assert max(shares) - min(shares) <= 2 * per_row.max() + 1e-9
+    for oi_bits in (0, 8, 32):  # CER; CSER with u8 / u32 omegaI (counted per segment)
+        for parts in (1, 2, 3, 8):
+            b = (ctypes.c_int64 * (parts + 1))()
+            assert L.cerdot_shard_plan(row_ptr.ctypes.data, 32, omega_ptr.ctypes.data, 32, 16, oi_bits, m, parts,
+                                       b) == 0
+            bounds = list(b)
+            assert bounds[0] == 0 and bounds[-1] == m and all(x <= y for x, y in zip(bounds, bounds[1:]))
+            per_row = np.array([2 * (omega_ptr[row_ptr[r + 1]] - omega_ptr[row_ptr[r]]) + (4 + oi_bits // 8) * segs[r]
+                                + 4 for r in range(m)], dtype=float)
+            shares = [per_row[a:c].sum() for a, c in zip(bounds[:-1], bounds[1:])]
+            assert max(shares) - min(shares) <= 2 * per_row.max() + 1e-9
     b = (ctypes.c_int64 * 2)()
-    assert L.cerdot_shard_plan(row_ptr.ctypes.data, 32, omega_ptr.ctypes.data, 32, 16, m, 0, b) == _native.E_VALUE
+    assert L.cerdot_shard_plan(row_ptr.ctypes.data, 32, omega_ptr.ctypes.data, 32, 16, 0, m, 0, b) == _native.E_VALUE
     with pytest.raises(ValueError):
         _native.check(_native.E_VALUE)
 

@@ -141,3 +141,15 @@ def test_uneven_blocks_are_padded_for_all_gather():
     # RowShardedDot pads short blocks to the longest; world of 1 short-circuits
     op = shard.RowShardedDot(object(), [4], compute=lambda enc, x: torch.arange(4.0))
     assert op(torch.zeros(3)).tolist() == [0.0, 1.0, 2.0, 3.0]
+
+
+@pytest.mark.parametrize("kind", ["cer", "cser"])
+def test_row_sharded_dot_world4_global_encoding(tmp_path, kind):
+    """bench.py's N>1 layout at world 4: one GLOBAL encoding (one alphabet), byte-balanced row slices of it
+    (the planner counts CSER omegaI bytes), y assembled by the all-gather: sharded == unsharded bitwise."""
+    out = str(tmp_path / "y4.npy")
+    mp.spawn(_worker, args=(4, _free_port(), kind, True, out), nprocs=4, join=True)
+    w, xs = synth.make_layer("oracle")
+    x = np.stack([xs[1], -xs[1], 2 * xs[1]], axis=1).astype(np.float64)
+    ref = c_oracle.dot(_as_dict(_host_encoding(kind, w)), x)
+    assert np.array_equal(np.load(out), ref)
