@@ -328,7 +328,66 @@ def _dot_host(a, xv: np.ndarray) -> np.ndarray:
     return y.reshape(a.m, 1) if (xv.ndim == 2 and batch == 1) else y
 
 
+class _FastHost(threading.local):
+    """Per-thread cache of the e2e host path's fixed call arguments per (encoding, input shape): pinned
+    staging views, the device workspace and the prebound C call, so a call is copy-in, one C call
+    (H2D, kernel, D2H, sync), copy-out."""
+
+    def __init__(self):
+        self.entries = {}
+
+
+_FAST = _FastHost()
+_F_TYPES = (np.float32, np.float64)
+
+
+def _raw_stream(idx: int) -> int:
+    return torch_mod()._C._cuda_getCurrentRawStream(idx)
+
+
+def _fast_entry(a, shape):
+    import weakref
+
+    torch = torch_mod()
+    batch = 1 if len(shape) == 1 else int(shape[1])
+    if _IO.dev is None:
+        _IO.dev = require_cuda()
+    dev = a._dev if a._dev is not None else a.device_encoding(_IO.dev)
+    if dev.device != _IO.dev:
+        _IO.dev, _IO.sets = dev.device, {}
+    idx = _IO.dev.index
+    st = dev.tile_struct(batch, torch._C._cuda_getCurrentRawStream(idx)) if batch > 1 else dev.struct()
+    L = _native.lib()
+    ws_bytes = L.cerdot_dot_host_workspace_bytes(st, batch)
+    px, px_np, py, py_np, ws = _IO.get(a.m, a.n, batch, ws_bytes)
+    call = (L.cerdot_dot_host, (ctypes.byref(st), ctypes.c_void_p(px.data_ptr()), batch, batch,
+                                 ctypes.c_void_p(py.data_ptr()), batch, ctypes.c_void_p(ws.data_ptr()), ws.numel()))
+    if len(_FAST.entries) > 64:
+        _FAST.entries.clear()
+    ent = (weakref.ref(a), px_np, py_np, call, idx, (a.m, 1) if len(shape) == 2 and batch == 1 else None,
+           (px, py, ws, st))
+    _FAST.entries[(id(a), shape)] = ent
+    return ent
+
+
+def _dot_host_fast(a, x: np.ndarray) -> np.ndarray:
+    """The e2e host path for numpy float32/float64 inputs: cached arguments (see _FastHost)."""
+    ent = _FAST.entries.get((id(a), x.shape))
+    if ent is None or ent[0]() is not a:
+        ent = _fast_entry(a, x.shape)
+    _, px_np, py_np, call, idx, shape2, _keep = ent
+    np.copyto(px_np, x.reshape(px_np.shape) if shape2 else x, casting="unsafe")  # the kernels compute in fp32
+    rc = call[0](*call[1], _raw_stream(idx))
+    if rc:
+        _native.check(rc)
+    y = py_np.astype(np.float64)
+    return y.reshape(shape2) if shape2 else y
+
+
 def _dot_encoded(a, x, trace, input_bits, output_bits, tracer):
+    if not trace and type(x) is np.ndarray and x.dtype.type in _F_TYPES and 1 <= x.ndim <= 2:
+        _check_shape(a.n, x.shape)
+        return _dot_host_fast(a, x)
     torch = torch_mod()
     if isinstance(x, torch.Tensor):
         _check_shape(a.n, tuple(x.shape))
@@ -364,6 +423,11 @@ def dot_cser(a: CserMatrix, x, trace: bool = False, input_bits: int | None = Non
 
 def dot(a, x, trace: bool = False, input_bits: int | None = None, output_bits: int | None = None):
     """Format-dispatched dot product (kernels.py:326-336)."""
+    if not trace and type(x) is np.ndarray and (type(a) is CerMatrix or type(a) is CserMatrix) and \
+            x.dtype.type in _F_TYPES and 1 <= x.ndim <= 2:
+        if x.shape[0] != a.n:
+            _check_shape(a.n, x.shape)
+        return _dot_host_fast(a, x)
     if isinstance(a, CerMatrix):
         return dot_cer(a, x, trace, input_bits, output_bits)
     if isinstance(a, CserMatrix):

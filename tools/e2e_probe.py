@@ -30,6 +30,9 @@ def main():
     enc = cd.encode_cer(w)
     out = {}
     out["public_dot_us"] = per_call(lambda: cd.dot(enc, x))
+    enc_s = cd.encode_cser(w)
+    out["public_dot_cser_us"] = per_call(lambda: cd.dot(enc_s, x))
+    out["public_step_us"] = per_call(lambda: (cd.dot(enc, x), cd.dot(enc_s, x)))
     dev = enc.device_encoding()
     st = dev.struct()
     L = _native.lib()
