@@ -584,21 +584,30 @@ __global__ void __launch_bounds__(NT, MINB) k_matvec(DotArgs a, const float *__r
       // ---- the whole row is in this window: lane i of a batch takes segment s0 + 32t + i, reads the
       // window prefix at its end and gets its start value (the previous segment's end) by shuffle
       uint32_t e_prev = w.e0;  // end of the previous segment
-      // segment [st, en): G(en - 1) - G(st - 1), both ends read from the tables by the segment's own lane
-      // (G before the row is 0: the masked gather zeroed the entries before e0)
+      float p_prev = 0.f;      // its lane-local prefix (entries before e0 were masked to 0)
+      // segment [st, en): G(en - 1) - G(st - 1), G = lane offset (hi, lo) + lane-local prefix; the lane-local
+      // prefix at st - 1 is the previous segment's end value (shuffled), the offsets come from the
+      // 32-entry table (one random prefix-table read per segment)
       auto seg = [&](uint32_t en, int k, bool valid) {
+        const bool has = valid && en > w0;
+        const float pe = has ? pre[ppos(en - 1u - w0)] : 0.f;
         uint32_t st = __shfl_up_sync(0xffffffffu, en, 1);
-        if (lane == 0) st = e_prev;
+        float ps = __shfl_up_sync(0xffffffffu, pe, 1);
+        if (lane == 0) {
+          st = e_prev;
+          ps = p_prev;
+        }
         e_prev = __shfl_sync(0xffffffffu, en, 31);
+        p_prev = __shfl_sync(0xffffffffu, pe, 31);
         if (valid && en > st) {
-          const GP ge = G(en - 1u - w0);
-          float d_hi = ge.hi, d_lo = ge.lo;
+          const float2 oe = off[(en - 1u - w0) >> 5];
+          float hi = oe.x, lo = oe.y + pe;
           if (st > w0) {
-            const GP gs = G(st - 1u - w0);
-            d_hi -= gs.hi;
-            d_lo -= gs.lo;
+            const float2 os = off[(st - 1u - w0) >> 5];
+            hi -= os.x;
+            lo -= os.y + ps;
           }
-          acc = fmaf(wv[k], d_hi + d_lo, acc);
+          acc = fmaf(wv[k], hi + lo, acc);
         }
       };
 #pragma unroll
