@@ -139,23 +139,64 @@ struct VecLoad<double, 2> {
 };
 
 // V elements per lane per step; V > 1 requires a contiguous, 16B-aligned matrix.
+// Counting: low-entropy matrices are dominated by one value (the background-to-be: 40-96% of the
+// elements in the BASELINE configs), so every thread counts the CTA's "hot" key -- the most frequent
+// key among the first 32 elements of the matrix -- in a register and sends only the other elements to
+// the shared-memory hash (atomics on ~4-60% of the elements, no warp-wide match per element).  The hot
+// guess only affects speed: its count is added like any other key's at the end.
 template <typename T, int V>
 __global__ void __launch_bounds__(256) k_value_hist(const T *__restrict__ w, int64_t m, int64_t n, int64_t ldw,
                                                     FastWs ws) {
   __shared__ unsigned long long skey[kLocalCap];
   __shared__ unsigned int scnt[kLocalCap];
+  __shared__ unsigned long long hot_sh;
+  __shared__ unsigned int hot_total;
   for (int i = threadIdx.x; i < kLocalCap; i += blockDim.x) {
     skey[i] = kEmptyKey;
     scnt[i] = 0;
   }
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t total = m * n;
   const bool contig = (ldw == n);
+  if (threadIdx.x < 32) {  // hot key: the mode of the first 32 elements (ties: lowest lane)
+    const int64_t e = lane;
+    unsigned long long kk = kEmptyKey;
+    if (e < total) {
+      const int64_t r = contig ? 0 : e / n;
+      kk = value_key(as_double(__ldg(w + (contig ? e : r * ldw + (e - r * n)))));
+    }
+    const unsigned int peers = __match_any_sync(0xffffffffu, kk);
+    const unsigned int c = kk == kEmptyKey ? 0u : static_cast<unsigned int>(__popc(peers));
+    unsigned int best = (c << 5) | (31u - lane);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    const unsigned long long hk = __shfl_sync(0xffffffffu, kk, 31 - static_cast<int>(best & 31u));
+    if (lane == 0) {
+      hot_sh = hk;
+      hot_total = 0;
+    }
+  }
+  __syncthreads();
+  const unsigned long long hot = hot_sh;
+  unsigned int hot_cnt = 0;
   const int64_t nvec = ceil_div(total, V);
   const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   unsigned int saw_pos0 = 0, saw_neg0 = 0;
+  auto insert_local = [&](unsigned long long key) -> bool {  // false: the alphabet overflowed the on-chip path
+    uint32_t h = hash_key(key) & (kLocalCap - 1);
+    for (int probe = 0; probe < kLocalProbe; ++probe) {
+      unsigned long long cur = skey[h];
+      if (cur == kEmptyKey) cur = atomicCAS(&skey[h], kEmptyKey, key), cur = (cur == kEmptyKey) ? key : cur;
+      if (cur == key) {
+        atomicAdd(&scnt[h], 1u);
+        return true;
+      }
+      h = (h + 1) & (kLocalCap - 1);
+    }
+    return global_insert(ws.gkey, ws.gcnt, ws.ctrl, key, 1ull);
+  };
+  bool ok = true;
   for (int64_t base = warp_id * 32; base < nvec; base += nwarps * 32) {
     const int64_t vi = base + lane;
     // the grid-stride loop holds one 16 B load per lane: bring the lines of two steps ahead into L2
@@ -187,34 +228,143 @@ __global__ void __launch_bounds__(256) k_value_hist(const T *__restrict__ w, int
     }
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      const unsigned long long key = valid[j] ? value_key(vals[j]) : kEmptyKey;
-      if (valid[j] && vals[j] == 0.0) {
+      if (!valid[j]) continue;
+      if (vals[j] == 0.0) {
         if (__double_as_longlong(vals[j]) < 0) saw_neg0 = 1; else saw_pos0 = 1;
       }
-      const unsigned int peers = __match_any_sync(0xffffffffu, key);
-      if (key != kEmptyKey && lane == __ffs(peers) - 1) {
-        const unsigned int cnt = __popc(peers);
-        uint32_t h = hash_key(key) & (kLocalCap - 1);
-        bool done = false;
-        for (int probe = 0; probe < kLocalProbe; ++probe) {
-          unsigned long long cur = skey[h];
-          if (cur == kEmptyKey) cur = atomicCAS(&skey[h], kEmptyKey, key), cur = (cur == kEmptyKey) ? key : cur;
-          if (cur == key) {
-            atomicAdd(&scnt[h], cnt);
-            done = true;
-            break;
-          }
-          h = (h + 1) & (kLocalCap - 1);
-        }
-        if (!done) global_insert(ws.gkey, ws.gcnt, ws.ctrl, key, cnt);
-      }
+      const unsigned long long key = value_key(vals[j]);
+      if (key == hot) ++hot_cnt;
+      else if (ok) ok = insert_local(key);
     }
+    if (__any_sync(0xffffffffu, !ok)) break;  // overflowed: the plan switches to the sort path
   }
   if (__any_sync(0xffffffffu, saw_pos0) && lane == 0) atomicOr(&ws.ctrl->pos_zero, 1u);
   if (__any_sync(0xffffffffu, saw_neg0) && lane == 0) atomicOr(&ws.ctrl->neg_zero, 1u);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hot_cnt += __shfl_xor_sync(0xffffffffu, hot_cnt, o);
+  if (lane == 0 && hot_cnt) atomicAdd(&hot_total, hot_cnt);
   __syncthreads();
+  if (threadIdx.x == 0 && hot_total) global_insert(ws.gkey, ws.gcnt, ws.ctrl, hot, hot_total);
   for (int i = threadIdx.x; i < kLocalCap; i += blockDim.x)
     if (skey[i] != kEmptyKey) global_insert(ws.gkey, ws.gcnt, ws.ctrl, skey[i], scnt[i]);
+}
+
+// fp32 fast path of the histogram.  An fp32 value is keyed on chip by its 32 bits (+-0 folded to +0,
+// every NaN to one NaN: np.unique's equalities), an order-preserving map of the float, so the per-element
+// work is integer only; the CTA's distinct keys are converted to the 64-bit float64 keys of the global
+// table (value_key) once, when merged.  Same counting scheme as k_value_hist (hot key in registers).
+__device__ __forceinline__ uint32_t fkey32(uint32_t b) {
+  if ((b & 0x7fffffffu) == 0u) return 0x80000000u;                               // +-0 -> key of +0
+  if ((b & 0x7f800000u) == 0x7f800000u && (b & 0x007fffffu)) return 0xffffffffu;  // NaN -> above +inf
+  return (b >> 31) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float fkey32_value(uint32_t k) {
+  if (k == 0xffffffffu) return __int_as_float(0x7fc00000);
+  return __uint_as_float((k >> 31) ? (k & 0x7fffffffu) : ~k);
+}
+constexpr uint32_t kEmpty32 = 0x7fffffffu;  // key of a negative NaN bit pattern: never produced by fkey32
+
+// Shared-memory hash insert of one key (k_value_hist_f32's non-hot elements).  false: alphabet overflow.
+__device__ __forceinline__ bool hist32_insert(uint32_t *skey, unsigned int *scnt, FastWs ws, uint32_t key) {
+  uint32_t h = (key * 0x9E3779B1u) >> (32 - 11);  // kLocalCap = 2^11 slots
+  for (int probe = 0; probe < kLocalProbe; ++probe) {
+    uint32_t cur = skey[h];
+    if (cur == kEmpty32) {
+      cur = atomicCAS(&skey[h], kEmpty32, key);
+      if (cur == kEmpty32) cur = key;
+    }
+    if (cur == key) {
+      atomicAdd(&scnt[h], 1u);
+      return true;
+    }
+    h = (h + 1) & (kLocalCap - 1);
+  }
+  return global_insert(ws.gkey, ws.gcnt, ws.ctrl, value_key(static_cast<double>(fkey32_value(key))), 1ull);
+}
+
+__global__ void __launch_bounds__(256) k_value_hist_f32(const float4 *__restrict__ w4, int64_t nvec, FastWs ws) {
+  __shared__ uint32_t skey[kLocalCap];
+  __shared__ unsigned int scnt[kLocalCap];
+  __shared__ uint32_t hot_sh;
+  __shared__ unsigned int hot_total;
+  __shared__ uint32_t stage_all[8][256];  // per-warp staging of non-hot keys (8 per lane per step)
+  for (int i = threadIdx.x; i < kLocalCap; i += blockDim.x) {
+    skey[i] = kEmpty32;
+    scnt[i] = 0;
+  }
+  const int lane = threadIdx.x & 31;
+  uint32_t *stage = stage_all[threadIdx.x >> 5];
+  if (threadIdx.x < 32) {  // hot key: the mode of the first 32 elements
+    const float *w = reinterpret_cast<const float *>(w4);
+    const uint32_t kk = lane < nvec * 4 ? fkey32(__float_as_uint(__ldg(w + lane))) : kEmpty32;
+    const unsigned int peers = __match_any_sync(0xffffffffu, kk);
+    unsigned int best = ((kk == kEmpty32 ? 0u : __popc(peers)) << 5) | (31u - lane);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    const uint32_t hk = __shfl_sync(0xffffffffu, kk, 31 - static_cast<int>(best & 31u));
+    if (lane == 0) {
+      hot_sh = hk;
+      hot_total = 0;
+    }
+  }
+  __syncthreads();
+  const uint32_t hot = hot_sh;
+  unsigned int hot_cnt = 0, saw_pos0 = 0, saw_neg0 = 0;
+  bool ok = true;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec; v += 2 * stride) {
+    const float4 a = __ldg(w4 + v);
+    const bool two = v + stride < nvec;
+    const float4 b = two ? __ldg(w4 + v + stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint32_t bits[8] = {__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(a.z), __float_as_uint(a.w),
+                              __float_as_uint(b.x), __float_as_uint(b.y), __float_as_uint(b.z), __float_as_uint(b.w)};
+    uint32_t keys[8];
+    unsigned todo = 0;  // elements that are not the hot key: the rare, out-of-line path
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool in = j < 4 || two;
+      const uint32_t bb = bits[j];
+      if (in && (bb & 0x7fffffffu) == 0u) {
+        if (bb) saw_neg0 = 1; else saw_pos0 = 1;
+      }
+      keys[j] = fkey32(bb);
+      if (in) {
+        if (keys[j] == hot) ++hot_cnt;
+        else todo |= 1u << j;
+      }
+    }
+    // warp-cooperative insertion: the warp's non-hot keys are staged in shared memory and inserted one
+    // key per lane (a divergent per-lane loop serialised ~3 atomic chains per warp step)
+    const unsigned c = __popc(todo);
+    unsigned incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const unsigned total_keys = __shfl_sync(0xffffffffu, incl, 31);
+    if (total_keys) {
+      unsigned pos = incl - c;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (todo & (1u << j)) stage[pos++] = keys[j];
+      __syncwarp();
+      for (unsigned i = lane; i < total_keys; i += 32) ok = hist32_insert(skey, scnt, ws, stage[i]) && ok;
+      __syncwarp();
+    }
+    if (__any_sync(0xffffffffu, !ok)) break;  // overflowed: the plan switches to the sort path
+  }
+  if (__any_sync(0xffffffffu, saw_pos0) && lane == 0) atomicOr(&ws.ctrl->pos_zero, 1u);
+  if (__any_sync(0xffffffffu, saw_neg0) && lane == 0) atomicOr(&ws.ctrl->neg_zero, 1u);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hot_cnt += __shfl_xor_sync(0xffffffffu, hot_cnt, o);
+  if (lane == 0 && hot_cnt) atomicAdd(&hot_total, hot_cnt);
+  __syncthreads();
+  if (threadIdx.x == 0 && hot_total)
+    global_insert(ws.gkey, ws.gcnt, ws.ctrl, value_key(static_cast<double>(fkey32_value(hot))), hot_total);
+  for (int i = threadIdx.x; i < kLocalCap; i += blockDim.x)
+    if (skey[i] != kEmpty32)
+      global_insert(ws.gkey, ws.gcnt, ws.ctrl, value_key(static_cast<double>(fkey32_value(skey[i]))), scnt[i]);
 }
 
 // One CTA: order the alphabet and build the rank lookup table.
@@ -225,7 +375,9 @@ __global__ void __launch_bounds__(1024) k_alphabet(FastWs ws, int bg_mode, doubl
   __shared__ unsigned int n_distinct;
   __shared__ int bg_pos;                              // frequency position of the background, -1 if absent
   __shared__ unsigned int k_final, rcap;
+  unsigned long long *fkey = cnt;  // value keys of the final alphabet (reuses cnt after the ranking)
   Ctrl *ctrl = ws.ctrl;
+  if (ctrl->overflow) return;  // the plan switches to the sort path after its one host synchronisation
   if (threadIdx.x == 0) {
     n_distinct = 0;
     bg_pos = -1;
@@ -280,11 +432,13 @@ __global__ void __launch_bounds__(1024) k_alphabet(FastWs ws, int bg_mode, doubl
   }
   if (bp < 0 && threadIdx.x == 0) ws.omega_freq[0] = bg_value;
   __syncthreads();
+  for (int f = threadIdx.x; f < kf; f += blockDim.x) fkey[f] = value_key(ws.omega_freq[f]);
+  __syncthreads();
   // value-ascending position of every final element (CSER, formats.py:269-270)
   for (int f = threadIdx.x; f < kf; f += blockDim.x) {
-    const unsigned long long kf_key = value_key(ws.omega_freq[f]);
+    const unsigned long long kf_key = fkey[f];
     int pos = 0;
-    for (int g = 0; g < kf; ++g) pos += value_key(ws.omega_freq[g]) < kf_key;
+    for (int g = 0; g < kf; ++g) pos += fkey[g] < kf_key;
     ws.to_vpos[f] = pos;
   }
   __syncthreads();
@@ -332,6 +486,8 @@ __global__ void __launch_bounds__(kRowThreads) k_row_count(const T *__restrict__
                                                            int64_t ldw, FastWs ws) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint64_t red[96];
+  // both rank widths are launched without a host round trip; the one that does not match k exits
+  if (ws.ctrl->overflow || (ws.ctrl->k <= 256) != (sizeof(RankT) == 1)) return;
   const unsigned int rcap = ws.ctrl->rcap;
   const unsigned int k = ws.ctrl->k;
   unsigned long long *rkey = reinterpret_cast<unsigned long long *>(smem);
@@ -415,6 +571,87 @@ __global__ void __launch_bounds__(kRowThreads) k_row_count(const T *__restrict__
   }
 }
 
+// fp32 fast path of k_row_count (contiguous rows, n % 4 == 0): elements keyed by their 32 bits (fkey32)
+// against a 32-bit copy of the rank table built in shared memory from the 64-bit one, the background
+// short-circuited; per element: integer key, one probe, a packed rank store, a shared atomic when it
+// is not the background.
+template <typename RankT>
+__global__ void __launch_bounds__(kRowThreads) k_row_count_f32(const float *__restrict__ w, int64_t m, int64_t n,
+                                                               int64_t ldw, FastWs ws) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint64_t red[96];
+  if (ws.ctrl->overflow || (ws.ctrl->k <= 256) != (sizeof(RankT) == 1)) return;
+  const unsigned int rcap = 2 * CERDOT_FAST_K;  // sparse (>= 2x the 64-bit table): ~1 probe per lookup
+  const unsigned int k = ws.ctrl->k;
+  uint32_t *rkey = reinterpret_cast<uint32_t *>(smem);
+  unsigned int *hist = rkey + rcap;
+  unsigned short *rrank = reinterpret_cast<unsigned short *>(hist + CERDOT_FAST_K);
+  const int shift = 32 - __ffs(rcap) + 1;  // rcap is a power of two
+  const unsigned int rcap64 = ws.ctrl->rcap;
+  for (unsigned int q = threadIdx.x; q < rcap; q += blockDim.x) rkey[q] = kEmpty32;
+  __syncthreads();
+  uint32_t bg32 = kEmpty32;
+  for (unsigned int q = threadIdx.x; q < rcap64; q += blockDim.x) {
+    const unsigned long long k64 = ws.rkey[q];
+    if (k64 == kEmptyKey) continue;
+    const double v = key_value(k64);
+    const float f = static_cast<float>(v);
+    if (!(static_cast<double>(f) == v || (v != v))) continue;  // not an fp32 value: no element can match it
+    const uint32_t key = fkey32(__float_as_uint(f));
+    uint32_t h = (key * 0x9E3779B1u) >> shift;
+    while (atomicCAS(&rkey[h], kEmpty32, key) != kEmpty32) h = (h + 1) & (rcap - 1);
+    rrank[h] = static_cast<unsigned short>(ws.rrank[q]);
+  }
+  {
+    const double bgv = ws.ctrl->background;
+    const float f = static_cast<float>(bgv);
+    if (static_cast<double>(f) == bgv || bgv != bgv) bg32 = fkey32(__float_as_uint(f));
+  }
+  RankT *ranks = static_cast<RankT *>(ws.ranks);
+  (void)bg32;
+  auto rank_of = [&](uint32_t key) -> unsigned int {  // every element's key is in the table
+    uint32_t h = (key * 0x9E3779B1u) >> shift;
+    while (rkey[h] != key) h = (h + 1) & (rcap - 1);
+    return rrank[h];
+  };
+  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+    for (unsigned int q = threadIdx.x; q < k; q += blockDim.x) hist[q] = 0;
+    __syncthreads();
+    const float4 *wr = reinterpret_cast<const float4 *>(w + row * ldw);
+    RankT *rr = ranks + row * n;
+    const int64_t nv = n / 4;
+#pragma unroll 4
+    for (int64_t c = threadIdx.x; c < nv; c += blockDim.x) {
+      const float4 v = __ldg(wr + c);
+      const uint32_t rk0 = rank_of(fkey32(__float_as_uint(v.x))), rk1 = rank_of(fkey32(__float_as_uint(v.y)));
+      const uint32_t rk2 = rank_of(fkey32(__float_as_uint(v.z))), rk3 = rank_of(fkey32(__float_as_uint(v.w)));
+      if (rk0) atomicAdd(&hist[rk0], 1u);
+      if (rk1) atomicAdd(&hist[rk1], 1u);
+      if (rk2) atomicAdd(&hist[rk2], 1u);
+      if (rk3) atomicAdd(&hist[rk3], 1u);
+      if (sizeof(RankT) == 1)
+        reinterpret_cast<uint32_t *>(rr)[c] = (rk0 & 0xffu) | ((rk1 & 0xffu) << 8) | ((rk2 & 0xffu) << 16) | (rk3 << 24);
+      else
+        reinterpret_cast<uint2 *>(rr)[c] = make_uint2(rk0 | (rk1 << 16), rk2 | (rk3 << 16));
+    }
+    __syncthreads();
+    uint64_t nnz = 0, present = 0, last = 0;
+    for (unsigned int q = 1 + threadIdx.x; q < k; q += blockDim.x) {
+      const unsigned int h = hist[q];
+      nnz += h;
+      present += h > 0;
+      if (h) last = max(last, static_cast<uint64_t>(q));
+    }
+    block_reduce3(nnz, present, last, red);
+    if (threadIdx.x == 0) {
+      ws.row_stat[row] = nnz;
+      ws.row_stat[m + row] = last;
+      ws.row_stat[2 * m + row] = present;
+    }
+    __syncthreads();
+  }
+}
+
 // One CTA of 1024 threads: three exclusive scans over m rows (m+1 outputs each).
 __global__ void __launch_bounds__(1024) k_scan_rows(int64_t m, FastWs ws) {
   __shared__ uint64_t part[3][1024];
@@ -434,12 +671,26 @@ __global__ void __launch_bounds__(1024) k_scan_rows(int64_t m, FastWs ws) {
     for (int j = 0; j < 3; ++j) part[j][t] += v[j];
     __syncthreads();
   }
-  // largest per-row statistic (max over the same partition, then over threads)
+  // largest per-row statistic (max over the same partition, then a block max: one store, not 3072
+  // same-address atomics)
   {
+    __shared__ uint64_t mx_sh[3][32];
     uint64_t mx[3] = {0, 0, 0};
     for (int64_t r = r0; r < r1; ++r)
       for (int j = 0; j < 3; ++j) mx[j] = max(mx[j], static_cast<uint64_t>(ws.row_stat[j * m + r]));
-    for (int j = 0; j < 3; ++j) atomicMax(&ws.ctrl->max_stat[j], static_cast<unsigned long long>(mx[j]));
+    for (int j = 0; j < 3; ++j) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx[j] = max(mx[j], static_cast<uint64_t>(__shfl_xor_sync(0xffffffffu, mx[j], o)));
+      if ((t & 31) == 0) mx_sh[j][t >> 5] = mx[j];
+    }
+    __syncthreads();
+    if (t < 32)
+      for (int j = 0; j < 3; ++j) {
+        uint64_t v = mx_sh[j][t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = max(v, static_cast<uint64_t>(__shfl_xor_sync(0xffffffffu, v, o)));
+        if (t == 0) ws.ctrl->max_stat[j] = v;
+      }
   }
   uint64_t run[3];
   for (int j = 0; j < 3; ++j) run[j] = part[j][t] - s[j];
@@ -601,6 +852,13 @@ int launch_hist(const void *w, int64_t m, int64_t n, int64_t ldw, const FastWs &
   const int64_t total = m * n;
   constexpr int V = sizeof(T) == 4 ? 4 : 2;
   const bool vec_ok = (ldw == n) && (reinterpret_cast<uintptr_t>(w) % 16 == 0);
+  if (sizeof(T) == 4 && vec_ok && total % 4 == 0) {  // fp32, contiguous: integer keys on chip
+    const int64_t nvec = total / 4;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nvec, 256 * 8), num_sms() * 8)));
+    k_value_hist_f32<<<grid, 256, 0, st>>>(static_cast<const float4 *>(w), nvec, ws);
+    CERDOT_LAUNCH_CHECK();
+    return CERDOT_OK;
+  }
   const int64_t units = vec_ok ? ceil_div(total, V) : total;
   const int64_t want = ceil_div(units, 256 * 8);
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, num_sms() * 8)));
@@ -613,9 +871,23 @@ int launch_hist(const void *w, int64_t m, int64_t n, int64_t ldw, const FastWs &
 }
 
 template <typename T, typename RankT>
-int launch_row_count(const void *w, int64_t m, int64_t n, int64_t ldw, const FastWs &ws, unsigned int k,
-                     unsigned int rcap, cudaStream_t st) {
-  const size_t smem = rcap * (sizeof(unsigned long long) + sizeof(unsigned short)) + k * sizeof(unsigned int) + 16;
+int launch_row_count(const void *w, int64_t m, int64_t n, int64_t ldw, const FastWs &ws, cudaStream_t st) {
+  if (sizeof(T) == 4 && n % 4 == 0 && ldw % 4 == 0 && reinterpret_cast<uintptr_t>(w) % 16 == 0) {
+    constexpr unsigned int kRcapMax32 = 2 * CERDOT_FAST_K;
+    const size_t smem32 = kRcapMax32 * (sizeof(uint32_t) + sizeof(unsigned short)) + CERDOT_FAST_K * sizeof(unsigned int) + 16;
+    auto kern32 = k_row_count_f32<RankT>;
+    CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern32, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem32)));
+    int per_sm = 0;  // one full wave of CTAs (a partial second wave idled a third of the GPU)
+    CERDOT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern32, kRowThreads, smem32));
+    const int grid32 = static_cast<int>(std::min<int64_t>(m, static_cast<int64_t>(num_sms()) * std::max(per_sm, 1)));
+    kern32<<<grid32, kRowThreads, smem32, st>>>(static_cast<const float *>(w), m, n, ldw, ws);
+    CERDOT_LAUNCH_CHECK();
+    return CERDOT_OK;
+  }
+  // sized for the largest on-chip alphabet (k and the rank-table capacity are device-side values here)
+  constexpr unsigned int kRcapMax = 2 * CERDOT_FAST_K;
+  const size_t smem =
+      kRcapMax * (sizeof(unsigned long long) + sizeof(unsigned short)) + CERDOT_FAST_K * sizeof(unsigned int) + 16;
   auto kern = k_row_count<T, RankT>;
   CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = static_cast<int>(std::min<int64_t>(m, num_sms() * 8));
@@ -628,16 +900,15 @@ template <typename ColT, typename RankT>
 int launch_fill(int64_t m, int64_t n, const FastWs &ws, unsigned int k, bool cser, void *col, void *op, int op_bits,
                 void *oi, int oi_bits, cudaStream_t st) {
   const size_t smem = (kRowWarps + 3) * static_cast<size_t>(k) * sizeof(unsigned int);
-  const int grid = static_cast<int>(std::min<int64_t>(m, num_sms() * 8));
-  if (cser) {
-    auto kern = k_row_fill<ColT, RankT, true>;
+  auto go = [&](auto kern) -> int {
     CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int per_sm = 0;  // one full wave of CTAs over the rows (no partial tail wave)
+    CERDOT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, smem));
+    const int grid = static_cast<int>(std::min<int64_t>(m, static_cast<int64_t>(num_sms()) * std::max(per_sm, 1)));
     kern<<<grid, kRowThreads, smem, st>>>(m, n, ws, static_cast<ColT *>(col), op, op_bits, oi, oi_bits);
-  } else {
-    auto kern = k_row_fill<ColT, RankT, false>;
-    CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, kRowThreads, smem, st>>>(m, n, ws, static_cast<ColT *>(col), op, op_bits, oi, oi_bits);
-  }
+    return CERDOT_OK;
+  };
+  if (int rc = cser ? go(k_row_fill<ColT, RankT, true>) : go(k_row_fill<ColT, RankT, false>)) return rc;
   CERDOT_LAUNCH_CHECK();
   return CERDOT_OK;
 }
@@ -664,30 +935,28 @@ int encode_plan(const void *w, int dtype, int64_t m, int64_t n, int64_t ldw, int
   CERDOT_CUDA_CHECK(cudaMemsetAsync(ws.ctrl, 0, sizeof(Ctrl), st));
   int rc = dtype == CERDOT_F32 ? launch_hist<float>(w, m, n, ldw, ws, st) : launch_hist<double>(w, m, n, ldw, ws, st);
   if (rc) return rc;
-  Ctrl ctrl{};
-  CERDOT_CUDA_CHECK(cudaMemcpyAsync(&ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-  CERDOT_CUDA_CHECK(cudaStreamSynchronize(st));
-  if (ctrl.overflow)  // alphabet too large for the on-chip tables: sort-based path (encode_sort.cu)
-    return encode_sort_plan(w, dtype, m, n, ldw, bg_mode, bg_value, workspace, workspace_bytes, info, st);
+  // alphabet, ranks, row statistics and scans are queued without host round trips (each kernel exits
+  // when the histogram overflowed the on-chip path); one synchronisation at the end reads the sizes
   k_alphabet<<<1, 1024, 0, st>>>(ws, bg_mode, bg_value);
   CERDOT_LAUNCH_CHECK();
-  CERDOT_CUDA_CHECK(cudaMemcpyAsync(&ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-  CERDOT_CUDA_CHECK(cudaStreamSynchronize(st));
-  const unsigned int k = ctrl.k;
-  if (k <= 256)
-    rc = dtype == CERDOT_F32 ? launch_row_count<float, uint8_t>(w, m, n, ldw, ws, k, ctrl.rcap, st)
-                             : launch_row_count<double, uint8_t>(w, m, n, ldw, ws, k, ctrl.rcap, st);
-  else
-    rc = dtype == CERDOT_F32 ? launch_row_count<float, uint16_t>(w, m, n, ldw, ws, k, ctrl.rcap, st)
-                             : launch_row_count<double, uint16_t>(w, m, n, ldw, ws, k, ctrl.rcap, st);
+  rc = dtype == CERDOT_F32 ? launch_row_count<float, uint8_t>(w, m, n, ldw, ws, st)
+                           : launch_row_count<double, uint8_t>(w, m, n, ldw, ws, st);
+  if (rc) return rc;
+  rc = dtype == CERDOT_F32 ? launch_row_count<float, uint16_t>(w, m, n, ldw, ws, st)
+                           : launch_row_count<double, uint16_t>(w, m, n, ldw, ws, st);
   if (rc) return rc;
   k_scan_rows<<<1, 1024, 0, st>>>(m, ws);
   CERDOT_LAUNCH_CHECK();
+  Ctrl ctrl{};
   uint64_t totals[3];
+  CERDOT_CUDA_CHECK(cudaMemcpyAsync(&ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
   for (int j = 0; j < 3; ++j)
     CERDOT_CUDA_CHECK(
         cudaMemcpyAsync(&totals[j], ws.scan + j * (m + 1) + m, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   CERDOT_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (ctrl.overflow)  // alphabet too large for the on-chip tables: sort-based path (encode_sort.cu)
+    return encode_sort_plan(w, dtype, m, n, ldw, bg_mode, bg_value, workspace, workspace_bytes, info, st);
+  const unsigned int k = ctrl.k;
   info->k = k;
   info->nnz = static_cast<int64_t>(totals[0]);
   info->segments_cer = static_cast<int64_t>(totals[1]);
@@ -695,8 +964,6 @@ int encode_plan(const void *w, int dtype, int64_t m, int64_t n, int64_t ldw, int
   info->mode_index = ctrl.mode_index;
   info->background = ctrl.background;
   info->path = 0;
-  CERDOT_CUDA_CHECK(cudaMemcpyAsync(&ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-  CERDOT_CUDA_CHECK(cudaStreamSynchronize(st));
   info->max_row_nnz = static_cast<int64_t>(ctrl.max_stat[0]);
   info->max_row_segments_cer = static_cast<int64_t>(ctrl.max_stat[1]);
   info->max_row_segments_cser = static_cast<int64_t>(ctrl.max_stat[2]);
