@@ -145,8 +145,15 @@ class _Encoded:
 
     # ---- device side
     def device_encoding(self, device=None) -> DeviceEncoding:
-        """The HBM-resident encoding (uploaded from the host arrays on first use)."""
+        """The HBM-resident encoding (uploaded from the host arrays on first use).
+
+        Host-constructed arrays are untrusted: they are validated on the device first (``validate``,
+        FormatError on a violation), because the kernels index x and shared memory with colI / omegaI
+        unchecked and an out-of-range index would fault the whole CUDA context (the reference raises
+        IndexError).  Encodings made by encode_* / read_matrix / the device slicer are device-resident from
+        the start and never take this path."""
         if self._dev is None:
+            validate(self)
             arrays = {"omega": self.omega, "colI": self.col_index, "omegaPtr": self.omega_ptr,
                       "rowPtr": self.row_ptr}
             if self._kind == _native.CSER:

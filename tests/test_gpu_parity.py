@@ -629,3 +629,18 @@ def test_device_row_slices_equal_host_slices():
                 ys.append(cd.dot(d, x))
             assert rel_err(torch.cat(ys).cpu().numpy(), y_full.double().cpu().numpy()) <= REL_TOL, (encode.__name__,
                                                                                                     parts)
+
+
+def test_untrusted_host_encoding_is_validated_before_the_kernels():
+    """A host-constructed encoding with an out-of-range column index raises FormatError at its first
+    device use (it would otherwise index x out of bounds inside the kernels); a valid one runs."""
+    w, xs = synth.make_layer("oracle")
+    ref = numpy_port.encode_cer(w)
+    good = cd.CerMatrix(ref["omega"], ref["colI"], ref["omegaPtr"], ref["rowPtr"], ref["m"], ref["n"])
+    assert rel_err(cd.dot(good, xs[1]), numpy_port.dot(ref, xs[1])) <= REL_TOL
+    col = np.array(ref["colI"]).copy()
+    col[5] = ref["n"] + 7
+    bad = cd.CerMatrix(ref["omega"], col, ref["omegaPtr"], ref["rowPtr"], ref["m"], ref["n"])
+    with pytest.raises(cd.FormatError):
+        cd.dot(bad, xs[1])
+    torch.cuda.synchronize()  # the context is intact
