@@ -279,7 +279,9 @@ def _graph_time(fn_step, steps: int, warmup: int, rotate: int, torch, sampler=No
     stream = torch.cuda.Stream()
     stream.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(stream):
-        for i in range(max(warmup, 3)):
+        # every rotating step runs at least once before capture: one-time setup (e.g. the mat-mat's tile
+        # view of each encoding copy) must not be captured into the timed graph
+        for i in range(max(warmup, 3, rotate)):
             fn_step(i % rotate)
     torch.cuda.current_stream().wait_stream(stream)
     torch.cuda.synchronize()

@@ -195,3 +195,21 @@ def test_tiled_and_flat_agree(name, batch):
             y_flat = cd.dot(enc, x).cpu().numpy()
         y_tiled = _tiled(enc, x).cpu().numpy()
         assert rel_err(y_tiled, y_flat) <= 2 * REL_TOL
+
+
+def test_tiled_skewed_rows():
+    """Power-law row lengths (a few dense rows, many near-empty ones): the entry-balanced row split per warp,
+    rows longer than a warp's 32-row pointer window, and empty (row, tile) lists, against the oracle."""
+    rng = np.random.default_rng(21)
+    m, n = 3000, 2500
+    dens = np.clip(rng.pareto(1.2, size=m) * 0.01, 0.0, 1.0)
+    dens[rng.choice(m, 40, replace=False)] = 0.0
+    levels = np.array([-0.3, -0.1, 0.2, 0.5, 1.5])
+    w = np.where(rng.random((m, n)) < dens[:, None], levels[rng.integers(0, 5, size=(m, n))], 0.0)
+    x = rng.standard_normal((n, 96)).astype(np.float32)
+    for kind, encode in (("cer", cd.encode_cer), ("cser", cd.encode_cser)):
+        enc = encode(w)
+        ref = c_oracle.dot(c_oracle.encode(w, kind), x.astype(np.float64))
+        for path in PATHS + ("flat",):
+            y = _tiled(enc, torch.from_numpy(x).cuda(), path).cpu().numpy()
+            assert rel_err(y, ref) <= REL_TOL, (kind, path)
