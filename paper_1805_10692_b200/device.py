@@ -109,6 +109,10 @@ class DeviceEncoding:
         hit = self._tile_views.get(nt)
         if hit is None:
             torch = torch_mod()
+            if torch.cuda.is_current_stream_capturing():
+                # building the view inside a user's CUDA-graph capture would make every replay rebuild it:
+                # use the flat kernel for this call (run one batched call before capturing to get the view)
+                return base
             tiles = -(-self.n // nt)
             tptr = torch.empty(tiles * self.m + 1, dtype=torch.int32, device=self.device)
             rec = torch.empty(max(1, self.nnz) * 2, dtype=torch.int32, device=self.device)

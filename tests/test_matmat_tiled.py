@@ -213,3 +213,26 @@ def test_tiled_skewed_rows():
         for path in PATHS + ("flat",):
             y = _tiled(enc, torch.from_numpy(x).cuda(), path).cpu().numpy()
             assert rel_err(y, ref) <= REL_TOL, (kind, path)
+
+
+def test_capture_before_the_view_exists_uses_the_flat_kernel():
+    """A first batched call inside a CUDA-graph capture does not capture the tile-view build: the replay
+    runs the flat kernel and gives the right answer; after an eager call, capture uses the tiled kernel."""
+    w, _ = synth.make_layer("resnet-conv")
+    x = torch.from_numpy(np.random.default_rng(8).standard_normal((w.shape[1], 96), dtype=np.float32)).cuda()
+    enc = cd.encode_cer(torch.from_numpy(w).cuda())
+    ref = c_oracle.dot(c_oracle.encode(w, "cer"), x.cpu().numpy().astype(np.float64))
+    for eager_first in (False, True):
+        if eager_first:
+            cd.dot_device(enc, x)
+            assert enc.device_encoding()._tile_views
+        y = torch.empty((w.shape[0], 96), device="cuda")
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+            cd.dot_device(enc, x, out=y)
+        g.replay()
+        torch.cuda.synchronize()
+        assert bool(enc.device_encoding()._tile_views) == eager_first
+        assert rel_err(y.cpu().numpy(), ref) <= REL_TOL
