@@ -383,13 +383,21 @@ __global__ void __launch_bounds__(1024) k_alphabet(FastWs ws, int bg_mode, doubl
     bg_pos = -1;
   }
   __syncthreads();
-  for (int s = threadIdx.x; s < kGlobalCap; s += blockDim.x) {
-    const unsigned long long kk = ws.gkey[s];
-    if (kk != kEmptyKey) {
-      const unsigned int idx = atomicAdd(&n_distinct, 1u);
-      key[idx] = kk;
-      cnt[idx] = ws.gcnt[s];
+  {  // all of this thread's slots loaded at once (8 independent loads, not 8 dependent round trips)
+    constexpr int kPer = kGlobalCap / 1024;
+    unsigned long long kk[kPer], cc[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      kk[j] = ws.gkey[threadIdx.x + j * 1024];
+      cc[j] = ws.gcnt[threadIdx.x + j * 1024];
     }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (kk[j] != kEmptyKey) {
+        const unsigned int idx = atomicAdd(&n_distinct, 1u);
+        key[idx] = kk[j];
+        cnt[idx] = cc[j];
+      }
   }
   __syncthreads();
   const int k0 = static_cast<int>(n_distinct);
@@ -654,53 +662,71 @@ __global__ void __launch_bounds__(kRowThreads) k_row_count_f32(const float *__re
 
 // One CTA of 1024 threads: three exclusive scans over m rows (m+1 outputs each).
 __global__ void __launch_bounds__(1024) k_scan_rows(int64_t m, FastWs ws) {
-  __shared__ uint64_t part[3][1024];
-  const int t = threadIdx.x;
+  // thread t owns rows [t*per, (t+1)*per); its row statistics are loaded in one batch (up to 8 rows x 3
+  // statistics in flight) before the block scan, then the outputs are written from registers
+  __shared__ uint64_t wsum[3][32];
+  __shared__ uint64_t mx_sh[3][32];
+  constexpr int kBatch = 8;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int64_t per = ceil_div(m, 1024);
   const int64_t r0 = min64(m, t * per), r1 = min64(m, r0 + per);
-  uint64_t s[3] = {0, 0, 0};
-  for (int64_t r = r0; r < r1; ++r)
-    for (int j = 0; j < 3; ++j) s[j] += ws.row_stat[j * m + r];
-  for (int j = 0; j < 3; ++j) part[j][t] = s[j];
-  __syncthreads();
-  // Hillis-Steele inclusive scan on 1024 partials (tiny)
-  for (int off = 1; off < 1024; off <<= 1) {
-    uint64_t v[3];
-    for (int j = 0; j < 3; ++j) v[j] = t >= off ? part[j][t - off] : 0;
-    __syncthreads();
-    for (int j = 0; j < 3; ++j) part[j][t] += v[j];
-    __syncthreads();
-  }
-  // largest per-row statistic (max over the same partition, then a block max: one store, not 3072
-  // same-address atomics)
-  {
-    __shared__ uint64_t mx_sh[3][32];
-    uint64_t mx[3] = {0, 0, 0};
-    for (int64_t r = r0; r < r1; ++r)
-      for (int j = 0; j < 3; ++j) mx[j] = max(mx[j], static_cast<uint64_t>(ws.row_stat[j * m + r]));
-    for (int j = 0; j < 3; ++j) {
+  uint64_t s[3] = {0, 0, 0}, mx[3] = {0, 0, 0};
+  for (int64_t b = r0; b < r1; b += kBatch) {
+    uint64_t v[3][kBatch];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx[j] = max(mx[j], static_cast<uint64_t>(__shfl_xor_sync(0xffffffffu, mx[j], o)));
-      if ((t & 31) == 0) mx_sh[j][t >> 5] = mx[j];
-    }
-    __syncthreads();
-    if (t < 32)
+    for (int i = 0; i < kBatch; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) v[j][i] = b + i < r1 ? ws.row_stat[j * m + b + i] : 0;
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i)
+#pragma unroll
       for (int j = 0; j < 3; ++j) {
-        uint64_t v = mx_sh[j][t];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = max(v, static_cast<uint64_t>(__shfl_xor_sync(0xffffffffu, v, o)));
-        if (t == 0) ws.ctrl->max_stat[j] = v;
+        s[j] += v[j][i];
+        mx[j] = max(mx[j], v[j][i]);
       }
   }
+  // block exclusive scan of the three sums; block max of the three maxima
+  uint64_t incl[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    incl[j] = s[j];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t u = __shfl_up_sync(0xffffffffu, incl[j], o);
+      if (lane >= o) incl[j] += u;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx[j] = max(mx[j], static_cast<uint64_t>(__shfl_xor_sync(0xffffffffu, mx[j], o)));
+    if (lane == 31) wsum[j][wid] = incl[j];
+    if (lane == 0) mx_sh[j][wid] = mx[j];
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      uint64_t w = wsum[j][lane], wi = w, mm = mx_sh[j][lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t u = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += u;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mm = max(mm, static_cast<uint64_t>(__shfl_xor_sync(0xffffffffu, mm, o)));
+      wsum[j][lane] = wi - w;  // exclusive warp offsets
+      if (lane == 31) ws.scan[j * (m + 1) + m] = wi;
+      if (lane == 0) ws.ctrl->max_stat[j] = mm;
+    }
+  }
+  __syncthreads();
   uint64_t run[3];
-  for (int j = 0; j < 3; ++j) run[j] = part[j][t] - s[j];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) run[j] = wsum[j][wid] + incl[j] - s[j];
   for (int64_t r = r0; r < r1; ++r)
+#pragma unroll
     for (int j = 0; j < 3; ++j) {
       ws.scan[j * (m + 1) + r] = run[j];
       run[j] += ws.row_stat[j * m + r];
     }
-  if (t == 1023)
-    for (int j = 0; j < 3; ++j) ws.scan[j * (m + 1) + m] = part[j][1023];
 }
 
 // Exclusive block scan of (a, b) pairs over the CTA; returns totals too.
