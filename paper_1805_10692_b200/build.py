@@ -16,8 +16,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libcerdot.so")
-SOURCES = ["abi.cu", "encode.cu", "encode_sort.cu", "dot.cu", "validate.cu", "lemx.cu", "tileview.cu", "synth.cu"]
-HEADERS = ["common.cuh", "encode.cuh", "tileview.cuh"]
+SOURCES = ["abi.cu", "encode.cu", "encode_sort.cu", "dot.cu", "dot_stream.cu", "validate.cu", "lemx.cu", "tileview.cu",
+           "synth.cu"]
+HEADERS = ["common.cuh", "encode.cuh", "tileview.cuh", "dotk.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
@@ -38,11 +39,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
     objs, cmds = [], []
+    common = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "cerdot.h"),
+                                                         os.path.abspath(__file__)]
     for src in SOURCES:
         obj = os.path.join(LIB_DIR, src.replace(".cu", ".o"))
+        objs.append(obj)
+        # an object is reused when it is newer than its source and every shared header
+        deps = [os.path.join(CSRC, src)] + common
+        if not force and os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in deps):
+            continue
         cmds.append([NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c",
                      os.path.join(CSRC, src), "-o", obj])
-        objs.append(obj)
     # the translation units compile in parallel (dot.cu alone is ~2 minutes)
     procs = []
     for cmd in cmds:

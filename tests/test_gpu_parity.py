@@ -170,7 +170,7 @@ def test_matmat_kernels_agree_bitwise(name, batch):
         assert torch.equal(y0, y1), (name, encode.__name__)
 
 
-@pytest.mark.parametrize("path", ["1", "2", "3"])
+@pytest.mark.parametrize("path", ["1", "2", "3", "4"])
 def test_u32_column_indices(kernel_path, path):
     """n > 65535 (u32 colI): every mat-vec kernel and the mat-mat kernel, integer alphabet -> bitwise."""
     kernel_path("matvec", int(path))
@@ -311,7 +311,7 @@ def test_wide_alphabets_up_to_fast_limit():
         assert np.array_equal(cd.dot(enc, x), w @ x)
 
 
-@pytest.mark.parametrize("path", ["tile", "window", "run"])
+@pytest.mark.parametrize("path", ["tile", "window", "run", "stream"])
 @pytest.mark.parametrize("name", ["oracle", "alexnet-fc6", "resnet-conv"])
 def test_matvec_paths_agree_with_oracle(kernel_path, config_goldens, name, path):
     """Every mat-vec kernel (CTA-tile TMA pipeline, warp-window kernel, 32-warp run kernel) meets the bar."""
@@ -325,7 +325,7 @@ def test_matvec_paths_agree_with_oracle(kernel_path, config_goldens, name, path)
         assert rel_err(cd.dot(enc, x1), ys[f"{name}/{kind}/b1"]) <= REL_TOL, (name, kind, path)
 
 
-@pytest.mark.parametrize("path", ["1", "2", "3"])
+@pytest.mark.parametrize("path", ["1", "2", "3", "4"])
 def test_matvec_tile_edge_rows(kernel_path, path):
     """Empty rows, single-entry rows, a long row next to short ones, non-zero background (every kernel)."""
     kernel_path("matvec", int(path))
@@ -378,7 +378,7 @@ def test_row_entry_index(name):
         re = dev.to_host("rowEntry")
         assert np.array_equal(re, enc.omega_ptr.astype(np.int64)[enc.row_ptr.astype(np.int64)])
         assert dev.struct().row_entry
-        for path in ("1", "2"):
+        for path in ("1", "2", "4"):
             from paper_1805_10692_b200._native import force_path
 
             with force_path("matvec", int(path)):
@@ -590,6 +590,8 @@ def test_randomized_round_trip_and_dot():
     mat-vec / mat-mat through every kernel path against the oracle (integer alphabets: bitwise)."""
     import os
 
+    from paper_1805_10692_b200._native import force_path
+
     rng = np.random.default_rng(int(os.environ.get("CERDOT_FUZZ_SEED", "1805")))
     for trial in range(int(os.environ.get("CERDOT_FUZZ_TRIALS", "60"))):
         m, n, kk = int(rng.integers(1, 70)), int(rng.integers(1, 400)), int(rng.integers(1, 9))
@@ -606,6 +608,9 @@ def test_randomized_round_trip_and_dot():
             assert np.array_equal(cd.decode(enc).values, w), (trial, kind)
             assert np.array_equal(cd.dot(enc, x), w @ x), (trial, kind)
             assert np.array_equal(cd.dot(enc, x[:, 0]), w @ x[:, 0]), (trial, kind)
+            for path in ("window", "tile", "run", "stream"):
+                with force_path("matvec", path):
+                    assert np.array_equal(cd.dot(enc, x[:, 1]), w @ x[:, 1]), (trial, kind, path)
 
 
 def test_device_row_slices_equal_host_slices():

@@ -77,7 +77,7 @@ def test_large_b256_rows_spread(large_layer):
             assert err <= REL_TOL, (kind, r0, err)
 
 
-@pytest.mark.parametrize("path", ["window", "run"])
+@pytest.mark.parametrize("path", ["window", "run", "stream"])
 def test_large_b1_every_row(large_layer, path):
     _, encs, refs, x = large_layer
     x1 = np.ascontiguousarray(x[:, 0])
@@ -96,7 +96,7 @@ def _b1_inputs(cfg):
             "ones": np.ones(cfg.n, dtype=np.float32)}
 
 
-@pytest.mark.parametrize("path", ["window", "tile", "run"])
+@pytest.mark.parametrize("path", ["window", "tile", "run", "stream"])
 @pytest.mark.parametrize("name", ["vgg-fc6", "resnet-conv", "alexnet-fc6"])
 def test_b1_relu_and_positive_inputs(name, path):
     cfg = synth.config(name)

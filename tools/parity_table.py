@@ -38,7 +38,7 @@ def main():
             ref_enc = c_oracle.encode(w, kind)
             for tag, x in inputs.items():
                 ref = c_oracle.dot(ref_enc, x.astype(np.float64))
-                for path in ("window", "tile", "run"):
+                for path in ("window", "tile", "run", "stream"):
                     with force_path("matvec", path):
                         y = cd.dot(enc, torch.from_numpy(x).cuda()).cpu().numpy()
                     out["b1"][f"{name}/{kind}/{tag}/{path}"] = err(y, ref)
@@ -65,7 +65,7 @@ def main():
     for kind, enc in encs.items():
         ref_enc = c_oracle.encode(wh, kind)
         ref1 = c_oracle.dot(ref_enc, x1.astype(np.float64))
-        for path in ("window", "run"):
+        for path in ("window", "run", "stream"):
             with force_path("matvec", path):
                 y = cd.dot(enc, torch.from_numpy(x1).cuda()).cpu().numpy()
             out["b1"][f"large/{kind}/own/{path}"] = err(y, ref1)
