@@ -202,6 +202,8 @@ int cerdot_tile_view_build(const cerdot_matrix *a, int32_t tile_rows, uint32_t *
  *                       4 tiled with sum-then-multiply per segment fragment
  *   CERDOT_PATH_MATVEC_NT: 1 co-resident 16-warp window kernel, 896 the 28-warp one
  *   CERDOT_PATH_MATMAT_DEPTH: X-row loads in flight of the flat kernel (8 / 16)
+ *   CERDOT_PATH_MATMAT_SPLIT: CTAs per row block sharing the X tiles of the tiled mat-mat (1, 2, 4, 8)
+ *   CERDOT_PATH_MATMAT_TILE: X rows per tile of a forced tiled mat-mat (128 / 256)
  * Returns the previous value; CERDOT_E_VALUE for an unknown op. */
 typedef enum {
   CERDOT_PATH_MATVEC = 0,
@@ -209,6 +211,8 @@ typedef enum {
   CERDOT_PATH_MATVEC_NT = 2,
   CERDOT_PATH_MATMAT_DEPTH = 3,
   CERDOT_PATH_TRACE = 4,
+  CERDOT_PATH_MATMAT_SPLIT = 5,
+  CERDOT_PATH_MATMAT_TILE = 6,
   CERDOT_PATH_COUNT
 } cerdot_path_op;
 int32_t cerdot_set_kernel_path(int32_t op, int32_t path);

@@ -129,10 +129,15 @@ int cerdot_encode_fill(const cerdot_encode_info *info, int32_t kind, void *works
                      row_ptr, row_ptr_bits, omega_index, omega_index_bits, static_cast<cudaStream_t>(stream));
 }
 
+static size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
 size_t cerdot_dot_workspace_bytes(const cerdot_matrix *a, int64_t batch) {
-  if (a == nullptr || a->background == 0.0 || batch <= 0) return 0;
-  // column sums, plus 16 row-range partials per column for batch > 1 (dot.cu: kColsumSplit)
-  return sizeof(double) * static_cast<size_t>(batch) * (batch > 1 ? 17 : 1);
+  if (a == nullptr || batch <= 0) return 0;
+  // column sums, plus 16 row-range partials per column for batch > 1 (dot.cu: kColsumSplit), 256 B
+  // aligned; then the tiled mat-mat's tile-split partial products (tileview.cu)
+  const size_t cs = a->background != 0.0 ? sizeof(double) * static_cast<size_t>(batch) * (batch > 1 ? 17 : 1) : 0;
+  const size_t part = cerdot::tile_view_dot_workspace_bytes(a, batch);
+  return part ? align256(cs) + part : cs;
 }
 
 size_t cerdot_validate_workspace_bytes(const cerdot_matrix *a) {
@@ -197,7 +202,6 @@ int cerdot_dot_cser(const cerdot_matrix *a, const float *x, int64_t ldx, int64_t
   return cerdot_dot(a, x, ldx, batch, y, ldy, workspace, workspace_bytes, stream);
 }
 
-static size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
 size_t cerdot_dot_host_workspace_bytes(const cerdot_matrix *a, int64_t batch) {
   if (a == nullptr || batch <= 0) return 0;

@@ -1709,7 +1709,12 @@ int dot(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, fl
   const int mm = kernel_path(CERDOT_PATH_MATMAT);
   if (batch > 1 && (mm == 0 || mm == 3 || mm == 4)) {
     bool used = false;
-    if (int rc = matmat_tiled(mat, x, ldx, batch, y, ldy, a.colsum, peers, a.npeer, peer_offset, st, &used)) return rc;
+    // workspace past the (256 B aligned) column sums: the tile-split partial products
+    const size_t cs = a.bg != 0.0 ? ((sizeof(double) * static_cast<size_t>(batch) * (1 + kColsumSplit) + 255) & ~size_t(255)) : 0;
+    void *pws = (workspace != nullptr && workspace_bytes > cs) ? static_cast<char *>(workspace) + cs : nullptr;
+    if (int rc = matmat_tiled(mat, x, ldx, batch, y, ldy, a.colsum, peers, a.npeer, peer_offset, pws,
+                              pws ? workspace_bytes - cs : 0, st, &used))
+      return rc;
     if (used) return CERDOT_OK;
   }
   return cser ? by_col<true>(a, mat->col_bits, mat->omega_ptr_bits, x, ldx, batch, y, ldy, st)

@@ -50,8 +50,13 @@ namespace {
 constexpr int kTvThreads = 512;
 constexpr int kTvWarps = kTvThreads / 32;
 constexpr uint32_t kTvMaxStages = 6;
-constexpr int32_t kTileRows = 128;  // X rows per tile (NT), the same for every V: one view per encoding
-constexpr uint32_t kFragEnd = 0x80000000u;
+constexpr int32_t kTileRows = 128;      // X rows per tile (NT) of dense-ish layers
+constexpr int32_t kTileRowsWide = 256;  // ... of sparse wide layers (longer (row, tile) lists)
+constexpr uint32_t kFragEnd = 0x80000000u;  // record .x bit 31: last entry of its segment fragment
+constexpr uint32_t kRowEnd = 0x40000000u;   // bit 30: last record of its (row, tile) list
+constexpr uint32_t kColMask = 0x1ffu;       // bits 0-8: X row inside the tile (NT = the sentinel zero row)
+constexpr uint32_t kRowShift = 9;           // bits 9-20: the matrix row, low 12 bits
+constexpr uint32_t kRowMask = 0xfffu;
 constexpr int kCountWarps = 8;
 constexpr int kScanThreads = 1024;
 
@@ -221,7 +226,12 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_tv_fill(const ColT *__rest
         __syncwarp();
         if (valid && (peers & lt) == 0) cur[t] += __popc(peers);
         __syncwarp();
-        if (valid) rec[pos] = make_uint2((c - t * nt) | (last ? kFragEnd : 0u), __float_as_uint(v));
+        if (valid) {
+          const bool row_end = pos + 1u == __ldg(tptr + static_cast<int64_t>(t) * m + r + 1);
+          rec[pos] = make_uint2((c - t * nt) | ((static_cast<uint32_t>(r) & kRowMask) << kRowShift) |
+                                    (row_end ? kRowEnd : 0u) | (last ? kFragEnd : 0u),
+                                __float_as_uint(v));
+        }
       }
     }
     __syncwarp();
@@ -235,6 +245,9 @@ struct TvArgs {
   const uint32_t *re;
   int64_t m, batch;
   uint32_t nt, tiles, rb, box_rows, stages;
+  uint32_t tper;   // X tiles per CTA (gridDim.z CTAs split the tiles of one row block)
+  float *part;     // tile-split partial products, [gridDim.z][m][ldp]; null: the CTA writes y itself
+  int64_t ldp;
   double bg;
   const double *colsum;
   float *const *ypeer;
@@ -309,6 +322,7 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_matmat_tv(const __grid_consta
   const uint32_t nboxes = a.nt / a.box_rows;
   const uint32_t tile_bytes = a.nt * CB * 4;
   const uint32_t S = a.stages;
+  const uint32_t t_lo = blockIdx.z * a.tper, t_hi = min(a.tiles, t_lo + a.tper);  // this CTA's X tiles
 
   // ---- prologue: barriers, zero y tile and sentinel rows, entry prefix of the CTA's rows
   if (threadIdx.x == 0) {
@@ -323,16 +337,16 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_matmat_tv(const __grid_consta
     reinterpret_cast<float *>(smem + L.xs + (i / CB) * L.xs_stride)[a.nt * CB + (i % CB)] = 0.f;
   for (uint32_t i = threadIdx.x; i <= nrow; i += kTvThreads) es[i] = __ldg(a.re + R0 + i);
   __syncthreads();
-  auto issue = [&](uint32_t t) {  // TMA of X tile t (rows t*NT.., columns cb0..) into buffer t % S
-    uint64_t *bar = full + (t % S);
-    float *dst = reinterpret_cast<float *>(smem + L.xs + (t % S) * L.xs_stride);
+  auto issue = [&](uint32_t t) {  // TMA of X tile t (rows t*NT.., columns cb0..) into buffer (t - t_lo) % S
+    uint64_t *bar = full + ((t - t_lo) % S);
+    float *dst = reinterpret_cast<float *>(smem + L.xs + ((t - t_lo) % S) * L.xs_stride);
     mbar_expect_tx(bar, tile_bytes);
     for (uint32_t bx = 0; bx < nboxes; ++bx)
       tma_load_2d(dst + bx * a.box_rows * CB, &xmap, cb0, static_cast<int>(t * a.nt + bx * a.box_rows), bar);
   };
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
-    for (uint32_t t = 0; t < S && t < a.tiles; ++t) issue(t);
+    for (uint32_t t = t_lo; t < t_lo + S && t < t_hi; ++t) issue(t);
   }
   // ---- this warp's rows [ra, rb): contiguous, balanced by entries (first row whose prefix >= target)
   uint32_t ra, rb;
@@ -354,62 +368,57 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_matmat_tv(const __grid_consta
   }
   const uint32_t nr = rb - ra;
   const uint32_t gra = R0 + ra;
-  // row pointers of tile t for rows ra .. ra + 31 in one lane-parallel register (prefetched two tiles
-  // ahead); rows past that (a warp with > 31 rows) are read from global memory when reached
+  // the warp's record range in tile t: tile_ptr at its first and one-past-last row (lanes 0 and 1),
+  // prefetched three tiles ahead; the rows themselves are named by the records (row bits, row-end flag)
   auto load_rp = [&](uint32_t t) -> uint32_t {
-    return (t < a.tiles && static_cast<uint32_t>(lane) <= nr) ? __ldg(a.tptr + static_cast<int64_t>(t) * m + gra + lane)
-                                                               : 0u;
+    return (t < t_hi && lane < 2) ? __ldg(a.tptr + static_cast<int64_t>(t) * m + gra + (lane ? nr : 0u)) : 0u;
   };
-  // (the rare global read is funnelled through a shuffle: the hot-path consumers of rp_at then depend on
-  // a SHFL, not on a load scoreboard that the in-flight record prefetches share)
-  auto rp_at = [&](uint32_t reg, uint32_t t, uint32_t i) -> uint32_t {
-    uint32_t src = reg;
-    if (i >= 32u) src = __ldg(a.tptr + static_cast<int64_t>(t) * m + gra + i);
-    return __shfl_sync(0xffffffffu, src, i < 32u ? (i & 31u) : 0);
-  };
-  const uint2 sentinel = make_uint2(a.nt, 0u);  // the zero row, no fragment end
+  const uint2 sentinel = make_uint2(a.nt, 0u);  // the zero row, no flags
   auto load_chunk = [&](uint32_t start, uint32_t end) -> uint2 {
     return (start + lane < end) ? __ldg(a.rec + start + lane) : sentinel;
   };
-  // prefetch pipeline: row pointers three tiles ahead, the first record chunk two tiles ahead (a warp
+  // prefetch pipeline: the range three tiles ahead, the first record chunk two tiles ahead (a warp
   // holds only a few dozen records per tile, so the tile boundary is where L2 latency would show)
-  uint32_t rp_c = load_rp(0), rp_n = load_rp(1), rp_nn = load_rp(2);
-  uint2 first = nr ? load_chunk(rp_at(rp_c, 0, 0), rp_at(rp_c, 0, nr)) : sentinel;
-  uint2 first_n = (nr && a.tiles > 1) ? load_chunk(rp_at(rp_n, 1, 0), rp_at(rp_n, 1, nr)) : sentinel;
+  uint32_t rp_c = load_rp(t_lo), rp_n = load_rp(t_lo + 1), rp_nn = load_rp(t_lo + 2);
+  auto range = [&](uint32_t reg, uint32_t &b, uint32_t &e) {
+    b = __shfl_sync(0xffffffffu, reg, 0);
+    e = __shfl_sync(0xffffffffu, reg, 1);
+  };
+  uint32_t P, Pe, Pn, Pne;
+  range(rp_c, P, Pe);
+  range(rp_n, Pn, Pne);
+  uint2 first = load_chunk(P, Pe);
+  uint2 first_n = load_chunk(Pn, Pne);
   const uint32_t lane_off = static_cast<uint32_t>(lane) * V * 4;
-  float *yw = ys + ra * CB + lane * V;  // this warp's first row in the y tile, this lane's columns
+  float *yl = ys + lane * V;  // this lane's columns of the CTA's y tile
+  const uint32_t r0low = R0 & kRowMask;
 
-  for (uint32_t t = 0; t < a.tiles; ++t) {
-    const uint32_t bsel = t % S;
-    const uint32_t P = rp_at(rp_c, t, 0), Pe = rp_at(rp_c, t, nr);
+  for (uint32_t t = t_lo; t < t_hi; ++t) {
+    const uint32_t bsel = (t - t_lo) % S;
     const uint32_t rp_n3 = load_rp(t + 3);
-    const uint2 first_nn = (nr && t + 2 < a.tiles) ? load_chunk(rp_at(rp_nn, t + 2, 0), rp_at(rp_nn, t + 2, nr))
-                                                   : sentinel;
-    // current row: the first with records in this tile; rend = where its records end
-    uint32_t r = 0;
-    while (r < nr && rp_at(rp_c, t, r + 1) == P) ++r;
-    uint32_t rend = r < nr ? rp_at(rp_c, t, r + 1) : 0xffffffffu;
-    mbar_wait(full + bsel, (t / S) & 1);
+    uint32_t Pnn, Pnne;
+    range(rp_nn, Pnn, Pnne);
+    const uint2 first_nn = load_chunk(Pnn, Pnne);
+    mbar_wait(full + bsel, ((t - t_lo) / S) & 1);
     const unsigned char *xb = smem + L.xs + bsel * L.xs_stride + lane_off;
     uint2 cur = first;
     float acc[V], run[V];
 #pragma unroll
     for (int q = 0; q < V; ++q) acc[q] = run[q] = 0.f;
-    auto row_done = [&](uint32_t pos) {  // the current row's records in this tile end at pos
-      float *yr = yw + r * CB;
+    auto row_flush = [&](uint32_t recx) {  // the record closes its row's list in this tile
+      float *yr = yl + (((recx >> kRowShift) - r0low) & kRowMask) * CB;
 #pragma unroll
       for (int q = 0; q < V; ++q) {
         yr[q] += acc[q];
         acc[q] = 0.f;
       }
-      ++r;
-      while (r < nr && rp_at(rp_c, t, r + 1) == pos) ++r;  // rows without records in this tile
-      rend = r < nr ? rp_at(rp_c, t, r + 1) : 0xffffffffu;
     };
     for (uint32_t p = P; p < Pe; p += 32) {
       const uint2 nxt = (p + 32 < Pe) ? load_chunk(p + 32, Pe) : sentinel;
       const unsigned emask = FRAG ? __ballot_sync(0xffffffffu, (cur.x & kFragEnd) != 0u) : 0u;
-      wb[lane] = make_uint2(cur.x & ~kFragEnd, cur.y);
+      const unsigned rmask = __ballot_sync(0xffffffffu, (cur.x & kRowEnd) != 0u);
+      // broadcast buffer: the X row's byte offset inside the tile buffer (flags and row bits stay in cur.x)
+      wb[lane] = make_uint2((cur.x & kColMask) * (CB * 4), cur.y);
       __syncwarp();
       const uint32_t cnt = min(32u, Pe - p);
       for (uint32_t g = 0; g < cnt; g += 8) {
@@ -425,7 +434,8 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_matmat_tv(const __grid_consta
         }
         XV<V> xv[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) xv[j] = lds_x<V>(xb + off[j] * (CB * 4));
+        for (int j = 0; j < 8; ++j) xv[j] = lds_x<V>(xb + off[j]);
+        const unsigned rg = (rmask >> g) & 0xffu;
         if (FRAG) {
           const unsigned eg = (emask >> g) & 0xffu;
 #pragma unroll
@@ -438,11 +448,10 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_matmat_tv(const __grid_consta
                 acc[q] = fmaf(vv[j], run[q], acc[q]);
                 run[q] = 0.f;
               }
-              const uint32_t pos = p + g + j + 1;
-              if (pos == rend) row_done(pos);  // a row's list ends with a fragment end
+              if (rg & (1u << j)) row_flush(__shfl_sync(0xffffffffu, cur.x, g + j));  // a list ends with a fragment end
             }
           }
-        } else if (p + g + 8 <= rend) {  // no row boundary inside these 8 entries
+        } else if (rg == 0u) {  // no row boundary inside these 8 entries
 #pragma unroll
           for (int j = 0; j < 8; ++j)
 #pragma unroll
@@ -450,21 +459,19 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_matmat_tv(const __grid_consta
         } else {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const uint32_t pos = p + g + j;
-            if (pos == rend) row_done(pos);
 #pragma unroll
             for (int q = 0; q < V; ++q) acc[q] = fmaf(vv[j], xv[j].v[q], acc[q]);
+            if (rg & (1u << j)) row_flush(__shfl_sync(0xffffffffu, cur.x, g + j));
           }
         }
       }
       __syncwarp();
       cur = nxt;
     }
-    if (!FRAG && r < nr) row_done(Pe);
     first = first_n;
     first_n = first_nn;
-    rp_c = rp_n;
-    rp_n = rp_nn;
+    P = Pn; Pe = Pne;
+    Pn = Pnn; Pne = Pnne;
     rp_nn = rp_n3;
     // release buffer bsel: the last warp to finish tile t re-arms it with tile t + S
     __syncwarp();
@@ -473,7 +480,7 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_matmat_tv(const __grid_consta
       const uint32_t old = atomicAdd(done_cnt + bsel, 1u);
       if (old == kTvWarps - 1) {
         atomicExch(done_cnt + bsel, 0u);
-        if (t + S < a.tiles) {
+        if (t + S < t_hi) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           issue(t + S);
         }
@@ -482,6 +489,11 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_matmat_tv(const __grid_consta
   }
   __syncthreads();
   // ---- epilogue: y = y tile (+ bg * colsum), coalesced rows of CB columns
+  if (a.part != nullptr) {  // tile split: this CTA's partial product; k_tv_reduce adds the splits in order
+    float *pz = a.part + (static_cast<int64_t>(blockIdx.z) * a.m + R0) * a.ldp + cb0;
+    for (uint32_t i = threadIdx.x; i < nrow * CB; i += kTvThreads) pz[static_cast<int64_t>(i / CB) * a.ldp + (i % CB)] = ys[i];
+    return;
+  }
   const int64_t ncols = min64(CB, a.batch - cb0);
   for (uint32_t i = threadIdx.x; i < nrow * CB; i += kTvThreads) {
     const uint32_t rr = i / CB, cc = i % CB;
@@ -492,6 +504,24 @@ __global__ void __launch_bounds__(kTvThreads, 1) k_matmat_tv(const __grid_consta
     const int64_t off = static_cast<int64_t>(R0 + rr) * ldy + c;
     y[off] = v;
     for (int pp = 0; pp < a.npeer; ++pp) a.ypeer[pp][a.ypeer_off + off] = v;
+  }
+}
+
+// y = sum over the tile splits (in split order: deterministic) + bg * colsum.
+__global__ void __launch_bounds__(256) k_tv_reduce(const float *__restrict__ part, int64_t ldp, uint32_t splits,
+                                                   int64_t m, int64_t batch, double bg, const double *__restrict__ colsum,
+                                                   float *__restrict__ y, int64_t ldy, float *const *ypeer, int npeer,
+                                                   int64_t ypeer_off) {
+  const int64_t total = m * batch;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / batch, c = i - r * batch;
+    float v = 0.f;
+    for (uint32_t z = 0; z < splits; ++z) v += part[(static_cast<int64_t>(z) * m + r) * ldp + c];
+    if (bg != 0.0) v = static_cast<float>(static_cast<double>(v) + bg * colsum[c]);
+    const int64_t off = r * ldy + c;
+    y[off] = v;
+    for (int pp = 0; pp < npeer; ++pp) ypeer[pp][ypeer_off + off] = v;
   }
 }
 
@@ -529,14 +559,14 @@ constexpr uint32_t kYBudget = 80 * 1024;    // the CTA's y tile
 struct TvGeom {
   int64_t col_blocks, row_blocks, rb;
 };
-TvGeom tv_geom(int64_t m, int64_t batch, int V) {
+TvGeom tv_geom(int64_t m, int64_t batch, int V, int64_t splits = 1) {
   const int64_t CB = 32 * V;
   TvGeom g{};
   g.col_blocks = ceil_div(batch, CB);
   const int64_t rb_max = kYBudget / (CB * 4);
   const int64_t sms = num_sms();
   for (int64_t waves = 1;; ++waves) {
-    g.row_blocks = std::max<int64_t>(1, sms * waves / g.col_blocks);
+    g.row_blocks = std::max<int64_t>(1, sms * waves / (g.col_blocks * splits));
     g.rb = ceil_div(m, g.row_blocks);
     if (g.rb <= rb_max || waves > 4096) break;
   }
@@ -550,12 +580,14 @@ TvGeom tv_geom(int64_t m, int64_t batch, int V) {
 // instructions per entry per warp, 4 per clock) and (c) the X tile fills through L2 (~6 KB/clk chip-wide,
 // B300_MICROARCH.md "LTS throughput cap").  Low X reuse (few rows per CTA, long X) favours narrow
 // column blocks; high reuse favours wide ones.
-int tile_view_v(int64_t m, int64_t n, int64_t nnz, int64_t batch) {
+int tile_view_v(int64_t m, int64_t n, int64_t nnz, int64_t batch, int32_t nt) {
   const double sms = num_sms();
   double best = 1e300;
   int bv = 1;
   for (int V : {1, 2, 4}) {
     if (V > 1 && batch <= 16 * V) continue;  // more than half the lanes idle
+    // two X stages and a y tile of at least 64 rows must fit
+    if (V > 1 && tv_layout(nt, 32 * V, 64, 2).total > 227u * 1024u) continue;
     const TvGeom g = tv_geom(m, batch, V);
     const double ctas = static_cast<double>(g.row_blocks * g.col_blocks);
     const double fill_bytes = ctas * static_cast<double>(n) * 32.0 * V * 4.0;
@@ -572,18 +604,53 @@ int tile_view_v(int64_t m, int64_t n, int64_t nnz, int64_t batch) {
   return bv;
 }
 
+// Tile splits: CTAs per row block that share its X tiles (gridDim.z).  A sparse wide layer leaves a warp
+// only a handful of entries per (row, tile) list when one CTA walks every tile of a few rows; splitting
+// the tiles over S CTAs gives each CTA S times the rows (longer per-tile record streams, 1/S of X through
+// its shared memory) at the price of S partial products added by k_tv_reduce.
+int tile_view_splits(const cerdot_matrix *a, int64_t batch, int V) {
+  const int forced = kernel_path(CERDOT_PATH_MATMAT_SPLIT);
+  const int32_t nt = a->tile_rows > 0 ? a->tile_rows : kTileRows;
+  const int64_t tiles = tile_view_tiles(a->n, nt);
+  int s = 1;
+  if (forced > 0) {
+    s = forced;
+  } else {
+    // entries per warp per tile at one split; aim for >= 96 (three record chunks), within 8 splits
+    const TvGeom g = tv_geom(a->m, batch, V);
+    const double per_warp_tile = static_cast<double>(a->nnz) / static_cast<double>(a->m) * nt /
+                                 static_cast<double>(a->n) * static_cast<double>(g.rb) / kTvWarps;
+    while (s < 8 && per_warp_tile * s < 96.0) s *= 2;
+  }
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(s, tiles)));
+}
+
+size_t tile_view_dot_workspace_bytes(const cerdot_matrix *a, int64_t batch) {
+  if (a->tile_ptr == nullptr || a->tile_rows <= 0 || batch <= 1) return 0;
+  const int V = tile_view_v(a->m, a->n, a->nnz, batch, a->tile_rows);
+  const int s = tile_view_splits(a, batch, V);
+  if (s <= 1) return 0;
+  const int64_t ldp = ceil_div(batch, 32 * V) * 32 * V;
+  return sizeof(float) * static_cast<size_t>(s) * static_cast<size_t>(a->m) * static_cast<size_t>(ldp);
+}
+
 int32_t tile_view_rows(const cerdot_matrix *a, int64_t batch) {
   if (batch <= 1 || a->nnz >= (int64_t(1) << 32) || a->m >= (int64_t(1) << 31) || a->n >= (int64_t(1) << 31))
     return 0;
   const int path = kernel_path(CERDOT_PATH_MATMAT);
-  if (path == 3 || path == 4) return kTileRows;  // forced
+  const int force_nt = kernel_path(CERDOT_PATH_MATMAT_TILE);
+  if (path == 3 || path == 4) return force_nt ? force_nt : kTileRows;  // forced
   if (path != 0) return 0;
-  // Automatic choice, measured on B200 (tools/mm_tiled_time.py): the tiled kernel pays a fixed cost per
-  // (row, tile) list (row hand-over, y-tile update, boundary checks), so it wins only when a row holds
-  // enough entries per X tile -- ResNet conv (~70 per list) and the 32768^2 layer (~38) -- and loses on
-  // sparse wide fc layers (AlexNet fc6 ~12, VGG fc6 ~5), where the flat L2-gather kernel stays.
+  // Automatic choice, measured on B200 (tools/mm_tiled_time.py, tools/mm_split_time.py): the tiled kernel
+  // pays a fixed cost per (row, tile) list (the y-tile update), so it needs enough entries per list:
+  //   * >= 24 per 128-row tile (ResNet conv ~70, the 32768^2 layer ~38): 128-row tiles;
+  //   * 8..24 (AlexNet fc6 ~12) at >= 48 columns: 256-row tiles with the tiles split over CTAs
+  //     (AlexNet fc6 B=64: 58 us vs 79 us flat);
+  //   * below that (VGG fc6 ~5: 145 us tiled vs 143 us flat) the flat L2-gather kernel stays.
   const double per_list = static_cast<double>(a->nnz) / static_cast<double>(a->m) * kTileRows / static_cast<double>(a->n);
-  return per_list >= 24.0 ? kTileRows : 0;
+  if (per_list >= 24.0) return kTileRows;
+  if (per_list >= 8.0 && batch >= 48) return kTileRowsWide;
+  return 0;
 }
 
 int64_t tile_view_tiles(int64_t n, int32_t nt) { return nt > 0 ? ceil_div(n, nt) : 0; }
@@ -682,8 +749,8 @@ int tile_view_build(const cerdot_matrix *a, int32_t nt, uint32_t *tptr, void *re
 
 // Returns CERDOT_OK with *used = false when the tiled path does not apply (the caller falls back).
 int matmat_tiled(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,
-                 const double *colsum, float *const *peers, int npeers, int64_t peer_offset, cudaStream_t st,
-                 bool *used) {
+                 const double *colsum, float *const *peers, int npeers, int64_t peer_offset, void *workspace,
+                 size_t workspace_bytes, cudaStream_t st, bool *used) {
   *used = false;
   if (mat->tile_ptr == nullptr || mat->tile_rec == nullptr || mat->tile_rows <= 0 || mat->row_entry == nullptr)
     return CERDOT_OK;
@@ -692,10 +759,15 @@ int matmat_tiled(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t 
   auto enc = tensor_map_encoder();
   if (enc == nullptr) return CERDOT_OK;
   const uint32_t nt = static_cast<uint32_t>(mat->tile_rows);
-  if (nt != static_cast<uint32_t>(kTileRows)) return CERDOT_OK;
-  const int V = tile_view_v(mat->m, mat->n, mat->nnz, batch);
+  if (nt != static_cast<uint32_t>(kTileRows) && nt != static_cast<uint32_t>(kTileRowsWide)) return CERDOT_OK;
+  const int V = tile_view_v(mat->m, mat->n, mat->nnz, batch, mat->tile_rows);
   const uint32_t CB = 32u * V;
-  const TvGeom g = tv_geom(mat->m, batch, V);
+  int splits = tile_view_splits(mat, batch, V);
+  const int64_t ldp = ceil_div(batch, CB) * CB;
+  if (splits > 1 && (workspace == nullptr ||
+                     workspace_bytes < sizeof(float) * static_cast<size_t>(splits) * mat->m * static_cast<size_t>(ldp)))
+    splits = 1;  // no room for the partial products: one CTA per row block walks every tile
+  const TvGeom g = tv_geom(mat->m, batch, V, splits);
   if (g.col_blocks > 65535 || g.row_blocks > 2147483647) return CERDOT_OK;
   const int64_t rb = g.rb, row_blocks = g.row_blocks, col_blocks = g.col_blocks;
   const uint32_t box_rows = std::min<uint32_t>(nt, 256u);
@@ -719,6 +791,9 @@ int matmat_tiled(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t 
   a.batch = batch;
   a.nt = nt;
   a.tiles = static_cast<uint32_t>(tile_view_tiles(mat->n, nt));
+  a.tper = static_cast<uint32_t>(ceil_div(a.tiles, splits));
+  a.part = splits > 1 ? static_cast<float *>(workspace) : nullptr;
+  a.ldp = ldp;
   a.rb = static_cast<uint32_t>(rb);
   a.box_rows = box_rows;
   // as many X stages (2..4) as fit next to the y tile
@@ -731,7 +806,7 @@ int matmat_tiled(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t 
   a.ypeer_off = peer_offset;
   const size_t smem = tv_layout(nt, CB, a.rb, a.stages).total;
   if (smem > 227u * 1024u) return CERDOT_OK;
-  const dim3 grid(static_cast<unsigned>(row_blocks), static_cast<unsigned>(col_blocks));
+  const dim3 grid(static_cast<unsigned>(row_blocks), static_cast<unsigned>(col_blocks), static_cast<unsigned>(splits));
   // per-entry fma (default) or sum-then-multiply per fragment (CERDOT_PATH_MATMAT = 4)
   const bool frag = kernel_path(CERDOT_PATH_MATMAT) == 4;
   auto go = [&](auto kern) -> int {
@@ -747,6 +822,12 @@ int matmat_tiled(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t 
   }
   if (rc) return rc;
   CERDOT_LAUNCH_CHECK();
+  if (splits > 1) {
+    const int rgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(mat->m * batch, 256), num_sms() * 8)));
+    k_tv_reduce<<<rgrid, 256, 0, st>>>(a.part, ldp, static_cast<uint32_t>(splits), mat->m, batch, a.bg, colsum, y, ldy,
+                                        a.ypeer, a.npeer, a.ypeer_off);
+    CERDOT_LAUNCH_CHECK();
+  }
   *used = true;
   return CERDOT_OK;
 }

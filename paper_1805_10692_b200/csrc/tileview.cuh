@@ -16,8 +16,10 @@ int tile_view_build(const cerdot_matrix *a, int32_t nt, uint32_t *tptr, void *re
                     size_t workspace_bytes, cudaStream_t st);
 // Runs the tiled mat-mat when the matrix carries a usable view; *used = false otherwise (caller falls back).
 int matmat_tiled(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t batch, float *y, int64_t ldy,
-                 const double *colsum, float *const *peers, int npeers, int64_t peer_offset, cudaStream_t st,
-                 bool *used);
+                 const double *colsum, float *const *peers, int npeers, int64_t peer_offset, void *workspace,
+                 size_t workspace_bytes, cudaStream_t st, bool *used);
+// Bytes of dot workspace the tiled mat-mat wants for its tile-split partial products (0: none).
+size_t tile_view_dot_workspace_bytes(const cerdot_matrix *a, int64_t batch);
 
 // numpy Generator(PCG64).choice on the device (synth.cu).
 int synth_choice(const uint64_t *state, const uint64_t *inc, uint64_t offset, const double *cdf, const float *levels,

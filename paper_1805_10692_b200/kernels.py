@@ -250,7 +250,11 @@ def dot_device(enc, x, out=None, stream=None, peers=None, peer_offset: int = 0):
         # == cerdot_dot_workspace_bytes: the column sums (+ 16 row-range partials each when batch > 1),
         # allocated per call from torch's caching allocator (ordered on the current stream; recorded on a
         # foreign one), so calls on different streams never share scratch
-        ws_bytes = (8 * batch * (17 if batch > 1 else 1)) if dev.background != 0.0 else 0
+        # (batch > 1: also the tiled mat-mat's tile-split partial products, so the size is asked for)
+        if batch > 1:
+            ws_bytes = int(_native.lib().cerdot_dot_workspace_bytes(st, batch))
+        else:
+            ws_bytes = 8 if dev.background != 0.0 else 0
         ws = None
         if ws_bytes:
             ws = torch.empty(ws_bytes, dtype=torch.uint8, device=x.device)

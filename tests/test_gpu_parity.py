@@ -143,9 +143,15 @@ def test_full_batch_resnet_conv_properties():
     w, xs = synth.make_layer(cfg)
     x = torch.from_numpy(xs[1568]).cuda()
     enc = cd.encode_cser(torch.from_numpy(w).cuda())
+    from paper_1805_10692_b200._native import force_path
+
     y = cd.dot(enc, x)
+    # per-column computation is independent of the batch at a fixed tile split (a narrow batch lets the
+    # automatic choice split the X tiles over CTAs, which re-associates the tile partial sums)
+    with force_path("matmat_split", 1):
+        assert torch.equal(cd.dot(enc, x)[:, 1000:1100], cd.dot(enc, x[:, 1000:1100].contiguous()))
     y_slice = cd.dot(enc, x[:, 1000:1100].contiguous())
-    assert torch.equal(y[:, 1000:1100], y_slice)  # per-column computation is independent of the batch
+    assert rel_err(y_slice.cpu().numpy(), y[:, 1000:1100].cpu().numpy()) <= 2e-6
     y2 = cd.dot(enc, 2.0 * x)
     assert torch.equal(y2, 2.0 * y)  # exact: scaling by 2 commutes with fp32 rounding
     ref = c_oracle.dot(c_oracle.encode(w, "cser"), xs[1568][:, 1500:].astype(np.float64))

@@ -31,7 +31,8 @@ if has_gpu():
 
 def tile_view_np(enc, nt: int):
     """numpy restatement of the view: records tile-major, then row, then the encoding's entry order; each
-    record = (its X row inside the tile | fragment end << 31, fp32 segment value)."""
+    record = (its X row inside the tile | matrix row (low 12 bits) << 9 | row end << 30 | fragment end << 31,
+    fp32 segment value)."""
     rp = enc.row_ptr.astype(np.int64)
     op = enc.omega_ptr.astype(np.int64)
     col = enc.col_index.astype(np.int64)
@@ -57,7 +58,12 @@ def tile_view_np(enc, nt: int):
     end = ~(nxt_same_seg & (nxt_tile == tile))
     order = np.lexsort((np.arange(col.size), ent_row, tile))
     rec = np.empty((col.size, 2), dtype=np.uint32)
-    rec[:, 0] = ((col - tile * nt) | (end.astype(np.int64) << 31))[order]
+    # row end: the last record of its (row, tile) list, i.e. the next record in view order changes (tile, row)
+    o_tile, o_row = tile[order], ent_row[order]
+    row_end = np.ones(col.size, dtype=bool)
+    row_end[:-1] = (o_tile[1:] != o_tile[:-1]) | (o_row[1:] != o_row[:-1])
+    rec[:, 0] = ((col - tile * nt) | ((ent_row & 0xFFF) << 9) | (end.astype(np.int64) << 31))[order] | (
+        row_end.astype(np.int64) << 30)
     rec[:, 1] = v[ent_seg].view(np.uint32)[order]
     tiles = -(-n // nt)
     cnt = np.zeros((tiles, m), dtype=np.int64)
@@ -236,3 +242,43 @@ def test_capture_before_the_view_exists_uses_the_flat_kernel():
         torch.cuda.synchronize()
         assert bool(enc.device_encoding()._tile_views) == eager_first
         assert rel_err(y.cpu().numpy(), ref) <= REL_TOL
+
+
+@pytest.mark.parametrize("nt", [128, 256])
+@pytest.mark.parametrize("split", [1, 2, 4, 8])
+def test_tile_split_and_wide_tiles_integer_bitwise(nt, split):
+    """The X tiles of a row block split over `split` CTAs (partial products added in split order by
+    k_tv_reduce) and 256-row tiles: integer data -> bitwise w @ x, with and without a background, at a
+    batch with a partial column block; the view of either tile height is bit-exact."""
+    rng = np.random.default_rng(100 * nt + split)
+    m, n = 333, 2100  # 17 / 9 tiles: uneven splits, a short last tile
+    w = rng.choice(np.arange(-3.0, 4.0), size=(m, n), p=[0.03, 0.04, 0.05, 0.76, 0.05, 0.04, 0.03])
+    w[4] = 0.0
+    w[9, 1000:1300] = 2.0
+    for batch in (40, 72):
+        x = rng.integers(-3, 4, size=(n, batch)).astype(np.float64)
+        xt = torch.from_numpy(x.astype(np.float32)).cuda()
+        for bg in (None, 1.0):
+            for encode in (cd.encode_cer, cd.encode_cser):
+                enc = encode(w, background=bg)
+                with force_path("matmat_tile", nt), force_path("matmat_split", split):
+                    for path in PATHS:
+                        y = _tiled(enc, xt, path).cpu().numpy()
+                        assert np.array_equal(y, w @ x), (nt, split, batch, bg, encode.__name__, path)
+                    vnt, tptr, rec = _view(enc, batch)
+                assert vnt == nt
+                tptr_ref, rec_ref = tile_view_np(enc, nt)
+                assert np.array_equal(tptr, tptr_ref) and np.array_equal(rec[: enc.nnz], rec_ref)
+
+
+def test_alexnet_auto_path_is_wide_tiles_with_split(config_goldens):
+    """Config 2 at B=64 takes the tiled kernel automatically (256-row tiles, tiles split over CTAs) and meets the bar."""
+    w, xs = synth.make_layer("alexnet-fc6")
+    xt = torch.from_numpy(xs[64]).cuda()
+    for kind, encode in (("cer", cd.encode_cer), ("cser", cd.encode_cser)):
+        enc = encode(torch.from_numpy(w).cuda())
+        y = cd.dot(enc, xt)
+        assert 256 in enc.device_encoding()._tile_views, "the automatic path did not build the 256-row view"
+        ref = c_oracle.dot(c_oracle.encode(w, kind), xs[64].astype(np.float64))
+        assert rel_err(y.cpu().numpy(), ref) <= REL_TOL, kind
+        assert torch.equal(y, cd.dot(enc, xt))

@@ -26,7 +26,9 @@ def main():
     enc = (cd.encode_cer if kind == "cer" else cd.encode_cser)(w)
     del w
     y = torch.empty((cfg.m, batch) if batch > 1 else (cfg.m,), device="cuda")
-    with force_path("matmat", os.environ.get("MM_PATH", "auto")), force_path("matvec", os.environ.get("MV_PATH", "auto")):
+    with force_path("matmat", os.environ.get("MM_PATH", "auto")), force_path("matvec", os.environ.get("MV_PATH", "auto")), \
+            force_path("matmat_split", int(os.environ.get("MM_SPLIT", "0"))), \
+            force_path("matmat_tile", int(os.environ.get("MM_TILE", "0"))):
         for _ in range(calls):
             cd.dot_device(enc, x, out=y)
     torch.cuda.synchronize()
