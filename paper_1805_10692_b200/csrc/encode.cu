@@ -861,6 +861,125 @@ __global__ void __launch_bounds__(kRowThreads) k_row_fill(int64_t m, int64_t n, 
   }
 }
 
+// CTA per row, u8 rank grid, n a multiple of 16: each warp first compacts the non-zero ranks of its column
+// slab into a shared list of (column << 8 | rank) entries in column order (16 ranks per lane per load,
+// one warp scan per 512 columns), so the per-rank counting and the stable scatter walk only the row's
+// entries instead of every column (a 91%-zero fc layer: 11x fewer steps; 130 -> ~45 us on AlexNet fc6).
+template <typename ColT, bool CSER>
+__global__ void __launch_bounds__(kRowThreads) k_row_fill_compact(int64_t m, int64_t n, FastWs ws, uint32_t cap,
+                                                                  ColT *__restrict__ col, void *omega_ptr, int op_bits,
+                                                                  void *omega_index, int oi_bits) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned int scan_sh[64];
+  const unsigned int k = ws.ctrl->k;
+  unsigned int *wc = reinterpret_cast<unsigned int *>(smem);  // [kRowWarps][k] per-warp counts -> offsets
+  unsigned int *cnt = wc + kRowWarps * k;                      // [k] per-rank count
+  unsigned int *excl = cnt + k;                                // [k] exclusive entry offset per rank
+  unsigned int *pidx = excl + k;                               // [k] CSER: index among present ranks
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t *list = reinterpret_cast<uint32_t *>(pidx + k) + static_cast<size_t>(wid) * cap;  // the warp's entries
+  const uint8_t *ranks = static_cast<const uint8_t *>(ws.ranks);
+  const uint64_t *entry_off = ws.scan;
+  const uint64_t *seg_off = ws.scan + (CSER ? 2 : 1) * (m + 1);
+  const int64_t slab = ceil_div(ceil_div(n, kRowWarps), 512) * 512;  // whole 512-column steps per warp
+  const unsigned int per = static_cast<unsigned int>(ceil_div(k, kRowThreads));
+  const unsigned int lt = (1u << lane) - 1u;
+  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+    for (unsigned int q = threadIdx.x; q < kRowWarps * k; q += blockDim.x) wc[q] = 0;
+    __syncthreads();
+    const uint8_t *rr = ranks + row * n;
+    const int64_t c_begin = wid * slab, c_end = min64(n, c_begin + slab);
+    // ---- compact: the warp's non-zero ranks, in column order
+    uint32_t nzw = 0;
+    for (int64_t c0 = c_begin; c0 < c_end; c0 += 512) {
+      const int64_t c = c0 + 16 * lane;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (c < c_end) v = *reinterpret_cast<const uint4 *>(rr + c);  // n % 16 == 0: whole vectors
+      const uint32_t wv4[4] = {v.x, v.y, v.z, v.w};
+      uint32_t nib[4], mine = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t nz = (((wv4[j] & 0x7f7f7f7fu) + 0x7f7f7f7fu) | wv4[j]) & 0x80808080u;
+        nib[j] = ((nz >> 7) * 0x01020408u) >> 24;  // bit b: byte b of the word is non-zero
+        mine += __popc(nib[j]);
+      }
+      uint32_t incl = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      uint32_t at = nzw + incl - mine;
+      nzw += __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t mk = nib[j];
+        while (mk) {
+          const int b = __ffs(static_cast<int>(mk)) - 1;
+          mk &= mk - 1u;
+          const uint32_t rk = (wv4[j] >> (8 * b)) & 0xffu;
+          list[at++] = (static_cast<uint32_t>(c + 4 * j + b) << 8) | rk;
+          atomicAdd(&wc[wid * k + rk], 1u);
+        }
+      }
+    }
+    __syncthreads();
+    // per rank: total count and per-warp exclusive offsets
+    for (unsigned int q = threadIdx.x; q < k; q += blockDim.x) {
+      unsigned int run = 0;
+#pragma unroll
+      for (int w2 = 0; w2 < kRowWarps; ++w2) {
+        const unsigned int v = wc[w2 * k + q];
+        wc[w2 * k + q] = run;
+        run += v;
+      }
+      cnt[q] = q == 0 ? 0 : run;
+    }
+    __syncthreads();
+    // block scan over ranks: thread t owns ranks [t*per, (t+1)*per)
+    unsigned int la = 0, lb = 0;
+    const unsigned int q0 = threadIdx.x * per, q1 = min(k, q0 + per);
+    for (unsigned int q = q0; q < q1; ++q) { la += cnt[q]; lb += cnt[q] > 0; }
+    unsigned int ea, eb;
+    block_exscan2(la, lb, ea, eb, scan_sh);
+    for (unsigned int q = q0; q < q1; ++q) {
+      excl[q] = ea;
+      pidx[q] = eb;
+      ea += cnt[q];
+      eb += cnt[q] > 0;
+    }
+    __syncthreads();
+    const uint64_t e0 = entry_off[row], s0 = seg_off[row];
+    const unsigned int last = static_cast<unsigned int>(ws.row_stat[m + row]);
+    for (unsigned int q = 1 + threadIdx.x; q < k; q += blockDim.x) {
+      const uint64_t end = e0 + excl[q] + cnt[q];
+      if (CSER) {
+        if (cnt[q]) {
+          const uint64_t j = s0 + pidx[q];
+          store_index(omega_index, oi_bits, j, ws.to_vpos[q]);
+          store_index(omega_ptr, op_bits, j + 1, end);
+        }
+      } else if (q <= last) {
+        store_index(omega_ptr, op_bits, s0 + q, end);  // segment s0 + q - 1 ends here
+      }
+    }
+    // stable scatter over the warp's entries: warp lists are column-ordered, lanes ordered inside a step
+    for (uint32_t i0 = 0; i0 < nzw; i0 += 32) {
+      const uint32_t e = i0 + lane < nzw ? list[i0 + lane] : 0u;
+      const unsigned int rk = e & 0xffu;
+      const unsigned int peers = __match_any_sync(0xffffffffu, rk);
+      if (rk != 0) {
+        const uint64_t pos = e0 + excl[rk] + wc[wid * k + rk] + __popc(peers & lt);
+        col[pos] = static_cast<ColT>(e >> 8);
+      }
+      __syncwarp();
+      if (rk != 0 && lane == __ffs(peers) - 1) wc[wid * k + rk] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
 // Tail: omega (CER frequency order / CSER value order), rowPtr, omegaPtr[0].
 __global__ void k_fill_tail(int64_t m, FastWs ws, bool cser, double *omega, void *row_ptr, int rp_bits,
                             void *omega_ptr, int op_bits) {
@@ -923,9 +1042,30 @@ int launch_row_count(const void *w, int64_t m, int64_t n, int64_t ldw, const Fas
 }
 
 template <typename ColT, typename RankT>
-int launch_fill(int64_t m, int64_t n, const FastWs &ws, unsigned int k, bool cser, void *col, void *op, int op_bits,
-                void *oi, int oi_bits, cudaStream_t st) {
+int launch_fill(int64_t m, int64_t n, const FastWs &ws, unsigned int k, int64_t max_row_nnz, int64_t nnz, bool cser, void *col,
+                void *op, int op_bits, void *oi, int oi_bits, cudaStream_t st) {
   const size_t smem = (kRowWarps + 3) * static_cast<size_t>(k) * sizeof(unsigned int);
+  // u8 ranks, whole 16 B vectors per row, columns that fit 24 bits, at most 20% non-zero (denser rows gain
+  // nothing from compaction: the 32768^2 layer at 30% ran 9.0 vs 7.3 ms): the compacting kernel, its
+  // per-warp entry lists sized by the longest row (a warp's slab cannot hold more), four CTAs per SM
+  if (sizeof(RankT) == 1 && (n % 16) == 0 && n < (int64_t(1) << 24) && nnz <= m * n / 5) {
+    const int64_t slab = ceil_div(ceil_div(n, kRowWarps), 512) * 512;
+    const uint32_t cap = static_cast<uint32_t>(std::min<int64_t>(slab, std::max<int64_t>(max_row_nnz, 1)));
+    const size_t smem_c = smem + sizeof(uint32_t) * kRowWarps * static_cast<size_t>(cap);
+    if (smem_c <= 56 * 1024) {
+      auto goc = [&](auto kern) -> int {
+        CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_c)));
+        int per_sm = 0;
+        CERDOT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, smem_c));
+        const int grid = static_cast<int>(std::min<int64_t>(m, static_cast<int64_t>(num_sms()) * std::max(per_sm, 1)));
+        kern<<<grid, kRowThreads, smem_c, st>>>(m, n, ws, cap, static_cast<ColT *>(col), op, op_bits, oi, oi_bits);
+        return CERDOT_OK;
+      };
+      if (int rc = cser ? goc(k_row_fill_compact<ColT, true>) : goc(k_row_fill_compact<ColT, false>)) return rc;
+      CERDOT_LAUNCH_CHECK();
+      return CERDOT_OK;
+    }
+  }
   auto go = [&](auto kern) -> int {
     CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;  // one full wave of CTAs over the rows (no partial tail wave)
@@ -1012,9 +1152,9 @@ int encode_fill(const cerdot_encode_info *info, int kind, void *workspace, size_
   auto by_col = [&](auto rank_tag) -> int {
     using RankT = decltype(rank_tag);
     switch (col_bits) {
-      case 8: return launch_fill<uint8_t, RankT>(m, n, ws, k, cser, col, op, op_bits, oi, oi_bits, st);
-      case 16: return launch_fill<uint16_t, RankT>(m, n, ws, k, cser, col, op, op_bits, oi, oi_bits, st);
-      default: return launch_fill<uint32_t, RankT>(m, n, ws, k, cser, col, op, op_bits, oi, oi_bits, st);
+      case 8: return launch_fill<uint8_t, RankT>(m, n, ws, k, info->max_row_nnz, info->nnz, cser, col, op, op_bits, oi, oi_bits, st);
+      case 16: return launch_fill<uint16_t, RankT>(m, n, ws, k, info->max_row_nnz, info->nnz, cser, col, op, op_bits, oi, oi_bits, st);
+      default: return launch_fill<uint32_t, RankT>(m, n, ws, k, info->max_row_nnz, info->nnz, cser, col, op, op_bits, oi, oi_bits, st);
     }
   };
   rc = k <= 256 ? by_col(uint8_t{}) : by_col(uint16_t{});
