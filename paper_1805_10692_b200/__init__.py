@@ -16,6 +16,7 @@ from .formats import (
     decode,
     encode_cer,
     encode_cser,
+    encode_pair,
     entry_count,
     index_bitwidth,
     storage_bits,
@@ -28,7 +29,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "DenseMatrix", "Vector", "CerMatrix", "CserMatrix", "FormatError", "array_bytes", "decode", "validate", "encode_cer",
-    "encode_cser", "entry_count", "index_bitwidth", "storage_bits", "OpTrace", "dot", "dot_cer", "dot_cser",
+    "encode_cser", "encode_pair", "entry_count", "index_bitwidth", "storage_bits", "OpTrace", "dot", "dot_cer", "dot_cser",
     "dot_device", "row_trace", "trace_cer", "trace_cser", "trace_of", "IoFormatError", "read_matrix",
     "write_matrix",
 ]

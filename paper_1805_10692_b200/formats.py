@@ -344,7 +344,9 @@ def _dense_source(a):
     return t, bits
 
 
-def _encode(a, kind: int, index_bits, background):
+def _plan(a, background):
+    """Shared first half of a conversion: alphabet, ranks, row statistics (one host synchronisation).
+    Returns what either format's fill needs; the workspace holds the rank grid until both are done."""
     torch = torch_mod()
     w, element_bits = _dense_source(a)
     m, n = int(w.shape[0]), int(w.shape[1])
@@ -366,6 +368,17 @@ def _encode(a, kind: int, index_bits, background):
             rc = L.cerdot_encode_plan(w.data_ptr(), dtype, m, n, n, bg_mode, bg_value, ws.data_ptr(), ws_bytes, info,
                                       st)
         _native.check(rc)
+    return w, element_bits, info, ws, ws_bytes
+
+
+def _fill(plan, kind: int, index_bits):
+    """Second half: allocate the encoding at the planned sizes and write its arrays."""
+    torch = torch_mod()
+    w, element_bits, info, ws, ws_bytes = plan
+    m, n = int(w.shape[0]), int(w.shape[1])
+    L = _native.lib()
+    with torch.cuda.device(w.device):
+        st = stream_ptr(w.device)
         segs = info.segments_cser if kind == _native.CSER else info.segments_cer
         bits = {"colI": _resolve_bits(max(n - 1, 0), index_bits)}
         if kind == _native.CSER:
@@ -385,10 +398,21 @@ def _encode(a, kind: int, index_bits, background):
     # background as stored in omega (CER omega[0]; CSER omega[mode_index]) — same value
     dev.background = float(info.background)
     dev._struct = None
-    del ws  # stream-ordered release through the caching allocator
     if kind == _native.CSER:
         return CserMatrix(None, None, None, None, None, m, n, element_bits, dev.mode_index, _device=dev)
     return CerMatrix(None, None, None, None, m, n, element_bits, _device=dev)
+
+
+def _encode(a, kind: int, index_bits, background):
+    return _fill(_plan(a, background), kind, index_bits)  # the workspace is released stream-ordered
+
+
+def encode_pair(a, index_bits="auto", background=None):
+    """(CerMatrix, CserMatrix) of the same matrix from ONE plan: the alphabet, the rank grid and the row
+    statistics are shared (formats.py:193-224 run once), only the two fills differ.  Equal, array by
+    array, to encode_cer(a) and encode_cser(a); an extension over the reference's API."""
+    plan = _plan(a, background)
+    return _fill(plan, _native.CER, index_bits), _fill(plan, _native.CSER, index_bits)
 
 
 def encode_cer(a, index_bits="auto", background=None) -> CerMatrix:

@@ -655,3 +655,24 @@ def test_untrusted_host_encoding_is_validated_before_the_kernels():
     with pytest.raises(cd.FormatError):
         cd.dot(bad, xs[1])
     torch.cuda.synchronize()  # the context is intact
+
+
+def test_encode_pair_equals_separate_encodes():
+    """encode_pair (one shared plan, two fills) == encode_cer and encode_cser array by array: a sparse fc
+    layer (compacting fill), a dense-ish one, an alphabet on the sort path, an explicit background."""
+    rng = np.random.default_rng(77)
+    big = rng.choice(rng.normal(size=3000), size=(40, 500))
+    big[rng.random(big.shape) < 0.4] = 0.0
+    cases = [(synth.make_layer("oracle")[0], None), (synth.make_layer("resnet-conv")[0], None), (big, None),
+             (synth.make_layer("oracle")[0], 0.25)]
+    for w, bg in cases:
+        wt = torch.from_numpy(w).cuda()
+        cer, cser = cd.encode_pair(wt, background=bg)
+        for got, want in ((cer, cd.encode_cer(wt, background=bg)), (cser, cd.encode_cser(wt, background=bg))):
+            assert type(got) is type(want)
+            for name in ("omega", "col_index", "omega_ptr", "row_ptr"):
+                assert np.array_equal(getattr(got, name), getattr(want, name)), (w.shape, bg, name)
+            if isinstance(got, cd.CserMatrix):
+                assert np.array_equal(got.omega_index, want.omega_index) and got.mode_index == want.mode_index
+        x = torch.from_numpy(rng.standard_normal(w.shape[1], dtype=np.float32)).cuda()
+        assert torch.equal(cd.dot(cer, x), cd.dot(cd.encode_cer(wt, background=bg), x))
