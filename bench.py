@@ -636,17 +636,20 @@ def run_ours(args):
             },
             "gmacs": round((1 if strong else world) * 2 * cfg.m * cfg.n / t_step / 1e9, 1),
             "roofline": {
-                "bound": "hbm", "kernel": "k_matvec<u16,u32,CER|CSER,896 threads> (the CER and CSER mat-vec)",
+                "bound": "hbm",
+                "kernel": ("k_matvec_row<u16,u32,CER|CSER> (the CER and CSER mat-vec, one row per warp)" if not strong
+                           else "k_matvec_stream<u16,u32,CER|CSER> (the long-row CER and CSER mat-vec)"),
                 "achieved": round(step_bytes / t_step / 1e9, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(step_bytes / t_step / 1e9 / peak, 4), "traffic": traffic.get("mean"),
                 "traffic_per_launch": traffic.get("per_launch"), "traffic_source": traffic.get("source"),
                 "peak_source": peak_src,
                 "per_launch_bytes": {"cer": alg_bytes(cer, 1), "cser": alg_bytes(cser, 1)},
-                "limiter": ("latency + the shared-memory pipe, not HBM: ~2.5 us of each ~7 us call pass before the "
+                "limiter": ("latency + the shared-memory pipe, not HBM: ~2.5 us of each ~6.7 us call pass before the "
                             "first gather (index chain, x staging), ~3 us are random x gathers from shared memory "
                             "(~3.4 bank-conflict ways) and segment lookups (DESIGN.md §3, tools/trace_matvec.py)"
                             if not strong else
-                            "the L1/shared data pipe (93% in ncu): x gathers + the colI ring (DESIGN.md §3)"),
+                            "instruction issue (76% of slots in ncu) next to the x gathers' shared-memory "
+                            "wavefronts (DESIGN.md §3)"),
             },
             "e2e": {"value": round(total_bytes / e2e_t / 1e9, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_t * 1e3, 4),

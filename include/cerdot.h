@@ -197,7 +197,8 @@ int cerdot_tile_view_build(const cerdot_matrix *a, int32_t tile_rows, uint32_t *
 /* Kernel selection override for A/B measurements and parity tests (process-wide; 0 = automatic, the
  * default).  Replaces reading environment variables on the dot path.
  *   CERDOT_PATH_MATVEC: 1 window kernel, 2 CTA-tile kernel, 3 long-row kernel (cp.async ring),
- *                       4 long-row stream kernel (register ring, fragment sums)
+ *                       4 long-row stream kernel (register ring, fragment sums),
+ *                       5 one-row-per-warp kernel (rows of at most one 1024-entry window)
  *   CERDOT_PATH_MATMAT: 1 flat L2-gather kernel, 2 per-segment kernel, 3 tiled (needs a view),
  *                       4 tiled with sum-then-multiply per segment fragment
  *   CERDOT_PATH_MATVEC_NT: 1 co-resident 16-warp window kernel, 896 the 28-warp one

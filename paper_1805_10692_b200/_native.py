@@ -112,7 +112,7 @@ _SIGNATURES = {
 # cerdot_path_op
 PATH_OPS = {"matvec": 0, "matmat": 1, "matvec_nt": 2, "matmat_depth": 3, "trace": 4, "matmat_split": 5, "matmat_tile": 6}
 # named kernel choices per op (the integers of include/cerdot.h)
-PATH_NAMES = {"matvec": {"auto": 0, "window": 1, "tile": 2, "run": 3, "stream": 4},
+PATH_NAMES = {"matvec": {"auto": 0, "window": 1, "tile": 2, "run": 3, "stream": 4, "row": 5},
               "matmat": {"auto": 0, "flat": 1, "segment": 2, "tiled": 3, "tiled_frag": 4}}
 
 _lib = None

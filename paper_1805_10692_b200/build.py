@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libcerdot.so")
-SOURCES = ["abi.cu", "encode.cu", "encode_sort.cu", "dot.cu", "dot_stream.cu", "validate.cu", "lemx.cu", "tileview.cu",
+SOURCES = ["abi.cu", "encode.cu", "encode_sort.cu", "dot.cu", "dot_stream.cu", "dot_row.cu", "validate.cu", "lemx.cu", "tileview.cu",
            "synth.cu"]
 HEADERS = ["common.cuh", "encode.cuh", "tileview.cuh", "dotk.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -51,57 +51,6 @@ namespace cerdot {
 namespace {
 
 
-constexpr int kEPL = 32;                      // entries per lane per window
-constexpr uint32_t kWin = 32 * kEPL;          // entries per window
-
-// Window-local prefix table of a warp: entry position p (lane p/32, item j=p%32) lives at
-// (j/4)*128 + lane*4 + j%4 so each lane writes its 32 prefixes as eight conflict-free 16 B stores.
-__device__ __forceinline__ uint32_t ppos(uint32_t p) { return ((p & 31u) >> 2) * 128u + (p >> 5) * 4u + (p & 3u); }
-
-// Gather x for one lane's 32 window entries (MASKED: only entries in [e0, e1)), build the lane's
-// running prefix sums and store them to the warp's prefix table; returns the lane total.
-template <typename ColT, bool XSMEM, bool MASKED>
-__device__ __forceinline__ float gather_prefix(const uint4 *raw_v, uint32_t w0, uint32_t e0, uint32_t e1,
-                                               const float *__restrict__ xs, const float *__restrict__ x, float *pre,
-                                               int lane) {
-  using CV = ColVec<ColT>;
-  constexpr int NV = kEPL / CV::kPer;
-  const uint32_t p0 = w0 + lane * kEPL;
-  uint32_t vmask = 0xffffffffu;
-  if (MASKED) {
-    const uint32_t jlo = e0 > p0 ? min(e0 - p0, 32u) : 0u;
-    const uint32_t jhi = e1 > p0 ? min(e1 - p0, 32u) : 0u;
-    vmask = (jhi >= 32u ? 0xffffffffu : ((1u << jhi) - 1u)) & ~(jlo >= 32u ? 0xffffffffu : ((1u << jlo) - 1u));
-  }
-  float run = 0.f;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    uint32_t c[CV::kPer];
-    CV::unpack(raw_v[v], c);
-#pragma unroll
-    for (int q = 0; q < CV::kPer / 4; ++q) {
-      float o[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int j = v * CV::kPer + q * 4 + t;
-        float g;
-        if (MASKED) {
-          g = 0.f;
-          if ((vmask >> j) & 1u) g = XSMEM ? xs[c[q * 4 + t]] : __ldg(x + c[q * 4 + t]);
-        } else {
-          g = XSMEM ? xs[c[q * 4 + t]] : __ldg(x + c[q * 4 + t]);
-        }
-        run += g;
-        o[t] = run;
-      }
-      const int jq = (v * CV::kPer + q * 4) >> 2;
-      *reinterpret_cast<float4 *>(pre + jq * 128 + lane * 4) = make_float4(o[0], o[1], o[2], o[3]);
-    }
-  }
-  return run;
-}
-
-
 // Shared-memory carve-up of k_matvec (byte offsets; all 16 B aligned).
 struct MatvecSmem {
   uint32_t bar, wv, pre, off, ring_op, ring_oi, xs, total;
@@ -1544,7 +1493,12 @@ int launch_dot(const DotArgs &a, const float *x, int64_t ldx, int64_t batch, flo
     // long rows (>= 4096 entries on average, the 32768^2 layer: 9829): the 32-warp run kernel
     // (431 -> 314 us there); at ~1000-entry rows (AlexNet, VGG fc6) the window kernel is 0-30% faster
     const bool long_rows = a.nnz >= int64_t(4096) * a.m;
-    const int want = force_path ? force_path : (few_rows ? 2 : (long_rows ? 4 : 1));
+    // one short row per warp (AlexNet fc6: 4096 rows of <= 1017 entries over 148 x 28 warps): the row kernel
+    const bool short_rows = a.max_row_nnz > 0 && matvec_row_fits(a, sizeof(ColT));
+    // (measured: AlexNet fc6 CER 7.26 -> 6.57 us, CSER 8.26 -> 6.91 us vs the window kernel; the 512 x 1024
+    // oracle layer 3.21 us vs 3.49 us for the tile pipeline)
+    const int want = force_path ? force_path : (short_rows ? 5 : (few_rows ? 2 : (long_rows ? 4 : 1)));
+    if (want == 5 && short_rows) return matvec_row(a, CSER, 8 * sizeof(ColT), 8 * sizeof(PtrT), x, y, st);
     if (tile_ok && want == 2) return launch_matvec_tile<ColT, PtrT, CSER>(a, x, y, st);
     // the stream kernel (dot_stream.cu): colI through registers, fragment sums, no prefix table
     if (want == 4 && a.nnz < (int64_t(1) << 32) - 65536 && matvec_stream_fits(a.k, a.n, 8 * sizeof(PtrT), CSER ? a.oi_bits : 0))

@@ -37,6 +37,10 @@ struct DotArgs {
   int64_t ypeer_off;
 };
 
+// The one-row-per-warp mat-vec (dot_row.cu).
+bool matvec_row_fits(const DotArgs &a, size_t col_bytes);
+int matvec_row(const DotArgs &a, bool cser, int col_bits, int op_bits, const float *x, float *y, cudaStream_t st);
+
 // The long-row mat-vec (dot_stream.cu).
 bool matvec_stream_fits(int64_t k, int64_t n, int op_bits, int oi_bits);
 int matvec_stream(const DotArgs &a, bool cser, int col_bits, int op_bits, const float *x, float *y, cudaStream_t st);
@@ -198,6 +202,58 @@ __device__ __forceinline__ void cp_async4(void *smem_dst, const void *gmem_src) 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int kEPL = 32;                      // entries per lane per window
+constexpr uint32_t kWin = 32 * kEPL;          // entries per window
+
+// Window-local prefix table of a warp: entry position p (lane p/32, item j=p%32) lives at
+// (j/4)*128 + lane*4 + j%4 so each lane writes its 32 prefixes as eight conflict-free 16 B stores.
+__device__ __forceinline__ uint32_t ppos(uint32_t p) { return ((p & 31u) >> 2) * 128u + (p >> 5) * 4u + (p & 3u); }
+
+// Gather x for one lane's 32 window entries (MASKED: only entries in [e0, e1)), build the lane's
+// running prefix sums and store them to the warp's prefix table; returns the lane total.
+template <typename ColT, bool XSMEM, bool MASKED>
+__device__ __forceinline__ float gather_prefix(const uint4 *raw_v, uint32_t w0, uint32_t e0, uint32_t e1,
+                                               const float *__restrict__ xs, const float *__restrict__ x, float *pre,
+                                               int lane) {
+  using CV = ColVec<ColT>;
+  constexpr int NV = kEPL / CV::kPer;
+  const uint32_t p0 = w0 + lane * kEPL;
+  uint32_t vmask = 0xffffffffu;
+  if (MASKED) {
+    const uint32_t jlo = e0 > p0 ? min(e0 - p0, 32u) : 0u;
+    const uint32_t jhi = e1 > p0 ? min(e1 - p0, 32u) : 0u;
+    vmask = (jhi >= 32u ? 0xffffffffu : ((1u << jhi) - 1u)) & ~(jlo >= 32u ? 0xffffffffu : ((1u << jlo) - 1u));
+  }
+  float run = 0.f;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    uint32_t c[CV::kPer];
+    CV::unpack(raw_v[v], c);
+#pragma unroll
+    for (int q = 0; q < CV::kPer / 4; ++q) {
+      float o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int j = v * CV::kPer + q * 4 + t;
+        float g;
+        if (MASKED) {
+          g = 0.f;
+          if ((vmask >> j) & 1u) g = XSMEM ? xs[c[q * 4 + t]] : __ldg(x + c[q * 4 + t]);
+        } else {
+          g = XSMEM ? xs[c[q * 4 + t]] : __ldg(x + c[q * 4 + t]);
+        }
+        run += g;
+        o[t] = run;
+      }
+      const int jq = (v * CV::kPer + q * 4) >> 2;
+      *reinterpret_cast<float4 *>(pre + jq * 128 + lane * 4) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+  return run;
+}
+
+
 
 }  // namespace
 }  // namespace cerdot

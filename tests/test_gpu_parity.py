@@ -176,7 +176,7 @@ def test_matmat_kernels_agree_bitwise(name, batch):
         assert torch.equal(y0, y1), (name, encode.__name__)
 
 
-@pytest.mark.parametrize("path", ["1", "2", "3", "4"])
+@pytest.mark.parametrize("path", ["1", "2", "3", "4", "5"])
 def test_u32_column_indices(kernel_path, path):
     """n > 65535 (u32 colI): every mat-vec kernel and the mat-mat kernel, integer alphabet -> bitwise."""
     kernel_path("matvec", int(path))
@@ -317,7 +317,7 @@ def test_wide_alphabets_up_to_fast_limit():
         assert np.array_equal(cd.dot(enc, x), w @ x)
 
 
-@pytest.mark.parametrize("path", ["tile", "window", "run", "stream"])
+@pytest.mark.parametrize("path", ["tile", "window", "run", "stream", "row"])
 @pytest.mark.parametrize("name", ["oracle", "alexnet-fc6", "resnet-conv"])
 def test_matvec_paths_agree_with_oracle(kernel_path, config_goldens, name, path):
     """Every mat-vec kernel (CTA-tile TMA pipeline, warp-window kernel, 32-warp run kernel) meets the bar."""
@@ -331,7 +331,7 @@ def test_matvec_paths_agree_with_oracle(kernel_path, config_goldens, name, path)
         assert rel_err(cd.dot(enc, x1), ys[f"{name}/{kind}/b1"]) <= REL_TOL, (name, kind, path)
 
 
-@pytest.mark.parametrize("path", ["1", "2", "3", "4"])
+@pytest.mark.parametrize("path", ["1", "2", "3", "4", "5"])
 def test_matvec_tile_edge_rows(kernel_path, path):
     """Empty rows, single-entry rows, a long row next to short ones, non-zero background (every kernel)."""
     kernel_path("matvec", int(path))
@@ -384,7 +384,7 @@ def test_row_entry_index(name):
         re = dev.to_host("rowEntry")
         assert np.array_equal(re, enc.omega_ptr.astype(np.int64)[enc.row_ptr.astype(np.int64)])
         assert dev.struct().row_entry
-        for path in ("1", "2", "4"):
+        for path in ("1", "2", "4", "5"):
             from paper_1805_10692_b200._native import force_path
 
             with force_path("matvec", int(path)):
@@ -614,7 +614,7 @@ def test_randomized_round_trip_and_dot():
             assert np.array_equal(cd.decode(enc).values, w), (trial, kind)
             assert np.array_equal(cd.dot(enc, x), w @ x), (trial, kind)
             assert np.array_equal(cd.dot(enc, x[:, 0]), w @ x[:, 0]), (trial, kind)
-            for path in ("window", "tile", "run", "stream"):
+            for path in ("window", "tile", "run", "stream", "row"):
                 with force_path("matvec", path):
                     assert np.array_equal(cd.dot(enc, x[:, 1]), w @ x[:, 1]), (trial, kind, path)
 
@@ -676,3 +676,28 @@ def test_encode_pair_equals_separate_encodes():
                 assert np.array_equal(got.omega_index, want.omega_index) and got.mode_index == want.mode_index
         x = torch.from_numpy(rng.standard_normal(w.shape[1], dtype=np.float32)).cuda()
         assert torch.equal(cd.dot(cer, x), cd.dot(cd.encode_cer(wt, background=bg), x))
+
+
+@pytest.mark.parametrize("name", ["alexnet-fc6", "oracle"])
+def test_row_kernel_bitwise_equals_window_kernel(name):
+    """The one-row-per-warp kernel runs the window kernel's single-window arithmetic: identical bits, on the
+    configs' own x, an all-positive x and a misaligned x view; and it is the automatic choice for AlexNet fc6."""
+    from paper_1805_10692_b200._native import force_path
+
+    w, xs = synth.make_layer(name)
+    rng = np.random.default_rng(8)
+    wt = torch.from_numpy(w).cuda()
+    pad = torch.zeros(w.shape[1] + 1, device="cuda")
+    for encode in (cd.encode_cer, cd.encode_cser):
+        enc = encode(wt)
+        for xv in (xs[1].reshape(-1), np.abs(rng.standard_normal(w.shape[1], dtype=np.float32))):
+            x = torch.from_numpy(xv).cuda()
+            with force_path("matvec", "window"):
+                y_win = cd.dot_device(enc, x)
+            with force_path("matvec", "row"):
+                y_row = cd.dot_device(enc, x)
+                pad[1:] = x
+                y_mis = cd.dot_device(enc, pad[1:])  # 4 B-aligned x: cooperative staging
+            assert torch.equal(y_win, y_row) and torch.equal(y_win, y_mis), (name, encode.__name__)
+            if name == "alexnet-fc6":
+                assert torch.equal(cd.dot_device(enc, x), y_row)

@@ -96,7 +96,7 @@ def _b1_inputs(cfg):
             "ones": np.ones(cfg.n, dtype=np.float32)}
 
 
-@pytest.mark.parametrize("path", ["window", "tile", "run", "stream"])
+@pytest.mark.parametrize("path", ["window", "tile", "run", "stream", "row"])
 @pytest.mark.parametrize("name", ["vgg-fc6", "resnet-conv", "alexnet-fc6"])
 def test_b1_relu_and_positive_inputs(name, path):
     cfg = synth.config(name)

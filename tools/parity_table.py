@@ -38,7 +38,7 @@ def main():
             ref_enc = c_oracle.encode(w, kind)
             for tag, x in inputs.items():
                 ref = c_oracle.dot(ref_enc, x.astype(np.float64))
-                for path in ("window", "tile", "run", "stream"):
+                for path in ("window", "tile", "run", "stream", "row"):
                     with force_path("matvec", path):
                         y = cd.dot(enc, torch.from_numpy(x).cuda()).cpu().numpy()
                     out["b1"][f"{name}/{kind}/{tag}/{path}"] = err(y, ref)
