@@ -31,7 +31,6 @@ namespace cerdot {
 
 namespace {
 
-constexpr int kStreamNT = 768;
 constexpr uint32_t kStreamWin = 256;   // entries per window, 8 per lane
 constexpr uint32_t kSegRing = 256;     // segment bounds held per warp (8 batches of 32)
 
@@ -511,12 +510,16 @@ int launch_stream(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
 
 template <typename ColT, typename PtrT, bool CSER>
 int by_flag(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
-  // CERDOT_PATH_MATVEC_NT = 1024 selects the 32-warp variant (A/B)
-  if (kernel_path(CERDOT_PATH_MATVEC_NT) == 1024)
+  // 32 warps at 64 registers (two colI windows in flight) for CER: 296 vs 309 us on the 32768^2 layer; the
+  // CSER instance spills at 64 registers (329 us) and stays at 24 warps (316 us).  CERDOT_PATH_MATVEC_NT =
+  // 768 / 1024 pins either (A/B).
+  const int want_nt = kernel_path(CERDOT_PATH_MATVEC_NT);
+  const bool wide = want_nt == 1024 || (want_nt != 768 && !CSER);
+  if (wide)
     return a.k <= 256 ? launch_stream<ColT, PtrT, CSER, uint8_t, 1024>(a, x, y, st)
                       : launch_stream<ColT, PtrT, CSER, uint16_t, 1024>(a, x, y, st);
-  return a.k <= 256 ? launch_stream<ColT, PtrT, CSER, uint8_t, kStreamNT>(a, x, y, st)
-                    : launch_stream<ColT, PtrT, CSER, uint16_t, kStreamNT>(a, x, y, st);
+  return a.k <= 256 ? launch_stream<ColT, PtrT, CSER, uint8_t, 768>(a, x, y, st)
+                    : launch_stream<ColT, PtrT, CSER, uint16_t, 768>(a, x, y, st);
 }
 
 template <typename ColT, bool CSER>
