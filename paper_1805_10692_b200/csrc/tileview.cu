@@ -8,16 +8,19 @@
 // (n x B) does not fit in shared memory, so X is cut into tiles of NT rows (the matrix's columns) and
 // every segment is split at the tile boundaries (colI is ascending inside a segment, formats.py:220, so
 // a segment's entries in tile t are one contiguous run: a "fragment").  The view lists, tile by tile and
-// row by row, every entry as one 8-byte record {column inside the tile | fragment-end flag, the
-// segment's value omega[k] - bg in fp32}, in the encoding's (rank, column) order:
+// row by row, every entry as one 8-byte record {column inside the tile | its row | row-end and
+// fragment-end flags, the segment's value omega[k] - bg in fp32}, in the encoding's (rank, column) order:
 //
 //   tile_ptr[t*m + r]   start of row r's records in tile t (tile-major; tile_ptr[T*m] = nnz)
-//   tile_rec[p]         .x = col - t*NT  (bit 31: last entry of its fragment), .y = float bits of v
+//   tile_rec[p]         .x = col - t*NT (bits 0-8) | (row & 0xfff) << 9 | bit 30: last record of its
+//                       (row, tile) list | bit 31: last entry of its fragment;  .y = float bits of v
 //
 // It is derived from colI / omegaPtr / rowPtr / omegaI once per encoding (k_tv_count, a scan, k_tv_fill)
 // and cached by the caller, like the rowEntry index; the format itself is unchanged.
 //
-// Kernel (k_matmat_tv).  CTA = (block of RB rows, 32*V batch columns), 16 warps, one CTA per SM:
+// Kernel (k_matmat_tv).  CTA = (block of RB rows, 32*V batch columns, one of S shares of the X tiles), 16
+// warps, one CTA per SM; with S > 1 a CTA writes a partial product and k_tv_reduce adds the S partials in
+// split order:
 //   * TMA (cp.async.bulk.tensor.2d, one elected thread) streams X tiles (NT rows x 32V columns,
 //     zero-filled past n and B) into a double buffer; the last warp to finish a tile re-arms its buffer;
 //   * warp w owns a contiguous range of the CTA's rows balanced by entries (rowEntry prefix), so its
@@ -25,8 +28,9 @@
 //     next chunk -- possibly the next tile's first -- is prefetched) and broadcast from shared memory;
 //   * per entry: one V-wide shared load of the X row, V adds into the fragment's running sums; at a
 //     fragment end one fma per column with the segment value (one multiply per fragment);
-//   * row partials accumulate in a shared y tile across the X tiles (each row owned by one warp: no
-//     atomics, fixed order); the epilogue adds bg * colsum(X) (fp64) and stores y (and to peers).
+//   * at a record with the row-end flag the warp adds its accumulators into the row's slot of a shared y
+//     tile (the row is named by the record: no row-pointer walk; each row owned by one warp: no atomics,
+//     fixed order); the epilogue adds bg * colsum(X) (fp64) and stores y (and to peers).
 // Summation order (the 1e-5 bar): per (row, column) fragments in (tile, rank, column) order, sequential
 // fp32 sums inside a fragment, one fp32 fma per fragment, tile partials added in tile order.
 // Deterministic: no floating-point atomics.
