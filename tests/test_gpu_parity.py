@@ -701,3 +701,34 @@ def test_row_kernel_bitwise_equals_window_kernel(name):
             assert torch.equal(y_win, y_row) and torch.equal(y_win, y_mis), (name, encode.__name__)
             if name == "alexnet-fc6":
                 assert torch.equal(cd.dot_device(enc, x), y_row)
+
+
+@pytest.mark.parametrize("levels", [9, 700])
+def test_stream_kernel_alphabets_modes_and_row_shapes(levels):
+    """The stream kernel on long rows with a small (u8 flags) and a wide (u16 flags) alphabet, a CSER mode in
+    the middle of the alphabet, empty rows, a row of one segment, rows ending exactly at a window boundary:
+    integer data -> bitwise w @ x; the same through the run and window kernels."""
+    from paper_1805_10692_b200._native import force_path
+
+    rng = np.random.default_rng(levels)
+    m, n = 37, 6000
+    vals = np.arange(-(levels // 2), levels - levels // 2).astype(np.float64)
+    p = rng.random(levels) + 0.05
+    p[levels // 2] += 0.6 * p.sum()  # a dominant value (0) in the middle of the sorted alphabet
+    w = rng.choice(vals, size=(m, n), p=p / p.sum())
+    w[3] = 0.0                     # empty row
+    w[5] = 4.0                     # one segment of n entries (23 full windows + a tail)
+    w[7, :] = 0.0
+    w[7, :2048] = 2.0              # ends exactly at a window boundary
+    w[9, 100:101] = -1.0
+    x = rng.integers(-2, 3, size=n).astype(np.float64)
+    for bg in (None, 1.0):
+        for encode in (cd.encode_cer, cd.encode_cser):
+            enc = encode(w, background=bg)
+            want = w @ x
+            for path in ("stream", "run", "window"):
+                with force_path("matvec", path):
+                    assert np.array_equal(cd.dot(enc, x), want), (levels, bg, encode.__name__, path)
+            for nt in (768, 1024):
+                with force_path("matvec", "stream"), force_path("matvec_nt", nt):
+                    assert np.array_equal(cd.dot(enc, x), want), (levels, bg, encode.__name__, nt)
