@@ -510,16 +510,15 @@ int launch_stream(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
 
 template <typename ColT, typename PtrT, bool CSER>
 int by_flag(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
-  // 32 warps at 64 registers (two colI windows in flight) for CER: 296 vs 309 us on the 32768^2 layer; the
-  // CSER instance spills at 64 registers (329 us) and stays at 24 warps (316 us).  CERDOT_PATH_MATVEC_NT =
-  // 768 / 1024 pins either (A/B).
-  const int want_nt = kernel_path(CERDOT_PATH_MATVEC_NT);
-  const bool wide = want_nt == 1024 || (want_nt != 768 && !CSER);
-  if (wide)
-    return a.k <= 256 ? launch_stream<ColT, PtrT, CSER, uint8_t, 1024>(a, x, y, st)
-                      : launch_stream<ColT, PtrT, CSER, uint16_t, 1024>(a, x, y, st);
-  return a.k <= 256 ? launch_stream<ColT, PtrT, CSER, uint8_t, 768>(a, x, y, st)
-                    : launch_stream<ColT, PtrT, CSER, uint16_t, 768>(a, x, y, st);
+  // 28 warps at <= 72 registers with two colI windows in flight (measured on the 32768^2 layer: CER 296 us,
+  // CSER 284 us; 24 warps with three windows 309 / 316 us; 32 warps at 64 registers 296 / 330 us -- the CSER
+  // instance then spills a ring slot, i.e. waits for the load it just issued).  CERDOT_PATH_MATVEC_NT = 768
+  // pins the 24-warp variant (A/B).
+  if (kernel_path(CERDOT_PATH_MATVEC_NT) == 768)
+    return a.k <= 256 ? launch_stream<ColT, PtrT, CSER, uint8_t, 768>(a, x, y, st)
+                      : launch_stream<ColT, PtrT, CSER, uint16_t, 768>(a, x, y, st);
+  return a.k <= 256 ? launch_stream<ColT, PtrT, CSER, uint8_t, 896>(a, x, y, st)
+                    : launch_stream<ColT, PtrT, CSER, uint16_t, 896>(a, x, y, st);
 }
 
 template <typename ColT, bool CSER>
@@ -544,7 +543,7 @@ int by_col(const DotArgs &a, int col_bits, int op_bits, const float *x, float *y
 
 bool matvec_stream_fits(int64_t k, int64_t n, int op_bits, int oi_bits) {
   if (k > kSmemValues || k < 1) return false;
-  return stream_layout(k, n, 1024 / 32, k <= 256 ? 1 : 2, op_bits / 8, oi_bits / 8).total <=
+  return stream_layout(k, n, 896 / 32, k <= 256 ? 1 : 2, op_bits / 8, oi_bits / 8).total <=
          static_cast<uint32_t>(kMaxSmemBytes);
 }
 

@@ -729,6 +729,6 @@ def test_stream_kernel_alphabets_modes_and_row_shapes(levels):
             for path in ("stream", "run", "window"):
                 with force_path("matvec", path):
                     assert np.array_equal(cd.dot(enc, x), want), (levels, bg, encode.__name__, path)
-            for nt in (768, 1024):
+            for nt in (768, 896):
                 with force_path("matvec", "stream"), force_path("matvec_nt", nt):
                     assert np.array_equal(cd.dot(enc, x), want), (levels, bg, encode.__name__, nt)
