@@ -309,32 +309,36 @@ __global__ void __launch_bounds__(256) k_value_hist_f32(const float4 *__restrict
   }
   __syncthreads();
   const uint32_t hot = hot_sh;
+  // The hot key as a test on raw bits: ((b ^ hb) & hm) == 0.  +-0 share a key (the sign is masked); a NaN
+  // hot key matches one NaN pattern only (other NaNs take the staged path and merge under the same key).
+  const bool hot_zero = hot == 0x80000000u;
+  const uint32_t hb = hot_zero ? 0u : (hot == 0xffffffffu ? 0x7fc00000u : __float_as_uint(fkey32_value(hot)));
+  const uint32_t hm = hot_zero ? 0x7fffffffu : 0xffffffffu;
   unsigned int hot_cnt = 0, saw_pos0 = 0, saw_neg0 = 0;
+  uint32_t hot_or = 0u, hot_and = 0xffffffffu;  // sign bits seen among the hot elements (+-0 bookkeeping)
   bool ok = true;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec; v += 2 * stride) {
     const float4 a = __ldg(w4 + v);
     const bool two = v + stride < nvec;
-    const float4 b = two ? __ldg(w4 + v + stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 b = two ? __ldg(w4 + v + stride) : a;  // no second vector: the first again, masked out below
     const uint32_t bits[8] = {__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(a.z), __float_as_uint(a.w),
                               __float_as_uint(b.x), __float_as_uint(b.y), __float_as_uint(b.z), __float_as_uint(b.w)};
-    uint32_t keys[8];
-    unsigned todo = 0;  // elements that are not the hot key: the rare, out-of-line path
+    unsigned todo = 0;  // elements that are not the hot key: the rare, staged path
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const bool in = j < 4 || two;
       const uint32_t bb = bits[j];
-      if (in && (bb & 0x7fffffffu) == 0u) {
-        if (bb) saw_neg0 = 1; else saw_pos0 = 1;
-      }
-      keys[j] = fkey32(bb);
-      if (in) {
-        if (keys[j] == hot) ++hot_cnt;
-        else todo |= 1u << j;
+      if (((bb ^ hb) & hm) != 0u) {
+        todo |= 1u << j;
+      } else {  // (a repeated first vector marks the same signs again: harmless)
+        hot_or |= bb;
+        hot_and &= bb;
       }
     }
-    // warp-cooperative insertion: the warp's non-hot keys are staged in shared memory and inserted one
-    // key per lane (a divergent per-lane loop serialised ~3 atomic chains per warp step)
+    if (!two) todo &= 0xfu;
+    hot_cnt += (two ? 8u : 4u) - __popc(todo);
+    // warp-cooperative insertion: the warp's non-hot elements are staged (raw bits) in shared memory and
+    // inserted one per lane (a divergent per-lane loop serialised ~3 atomic chains per warp step)
     const unsigned c = __popc(todo);
     unsigned incl = c;
 #pragma unroll
@@ -347,12 +351,22 @@ __global__ void __launch_bounds__(256) k_value_hist_f32(const float4 *__restrict
       unsigned pos = incl - c;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (todo & (1u << j)) stage[pos++] = keys[j];
+        if (todo & (1u << j)) stage[pos++] = bits[j];
       __syncwarp();
-      for (unsigned i = lane; i < total_keys; i += 32) ok = hist32_insert(skey, scnt, ws, stage[i]) && ok;
+      for (unsigned i = lane; i < total_keys; i += 32) {
+        const uint32_t bb = stage[i];
+        if ((bb & 0x7fffffffu) == 0u) {
+          if (bb) saw_neg0 = 1; else saw_pos0 = 1;
+        }
+        ok = hist32_insert(skey, scnt, ws, fkey32(bb)) && ok;
+      }
       __syncwarp();
     }
     if (__any_sync(0xffffffffu, !ok)) break;  // overflowed: the plan switches to the sort path
+  }
+  if (hot_zero && hot_cnt) {  // which zeros the hot elements were
+    if (hot_or >> 31) saw_neg0 = 1;
+    if (!(hot_and >> 31)) saw_pos0 = 1;
   }
   if (__any_sync(0xffffffffu, saw_pos0) && lane == 0) atomicOr(&ws.ctrl->pos_zero, 1u);
   if (__any_sync(0xffffffffu, saw_neg0) && lane == 0) atomicOr(&ws.ctrl->neg_zero, 1u);
