@@ -29,8 +29,10 @@ namespace {
 
 constexpr int kRowNT = 896;  // 28 warps per SM: a 4096-row layer has at most one row per warp on 148 SMs
 
+constexpr uint32_t kRowStage = 1024;  // results a CTA can stage for the fused exchange's coalesced peer stores
+
 struct RowSmem {
-  uint32_t bar, wv, pre, off, xs, total;
+  uint32_t bar, wv, pre, off, ystage, xs, total;
 };
 __host__ __device__ __forceinline__ RowSmem row_layout(int64_t k, int64_t n, uint32_t warps) {
   RowSmem L{};
@@ -44,12 +46,13 @@ __host__ __device__ __forceinline__ RowSmem row_layout(int64_t k, int64_t n, uin
   L.wv = take(static_cast<uint32_t>(k) * 4u);
   L.pre = take(warps * kWin * 4u);
   L.off = take(warps * 32u * 8u);
+  L.ystage = take(kRowStage * 4u);
   L.xs = take(static_cast<uint32_t>(n) * 4u);
   L.total = o;
   return L;
 }
 
-template <typename ColT, typename PtrT, bool CSER>
+template <typename ColT, typename PtrT, bool CSER, bool PEERS>
 __global__ void __launch_bounds__(kRowNT, 1) k_matvec_row(DotArgs a, const float *__restrict__ x,
                                                           float *__restrict__ y) {
   constexpr int kWarps = kRowNT / 32;
@@ -134,11 +137,22 @@ __global__ void __launch_bounds__(kRowNT, 1) k_matvec_row(DotArgs a, const float
   pdl_wait();  // y may be read or written by the producer grid
   bool ready = false;
   const float y_empty = a.bg != 0.0 ? static_cast<float>(a.bg * a.colsum[0]) : 0.f;
+  // Row-sharded exchange (peers): the CTA's rows are contiguous, so their results are staged in shared
+  // memory and written to y and to every peer's buffer as coalesced stores at the end (one 4-byte NVLink
+  // store per row per peer otherwise).  Without peers a result is stored as soon as its row is done.
+  const uint32_t cta_r0 = static_cast<uint32_t>(static_cast<uint64_t>(blockIdx.x) * kWarps * a.m / nw);
+  const uint32_t cta_r1 = static_cast<uint32_t>((static_cast<uint64_t>(blockIdx.x) + 1) * kWarps * a.m / nw);
+  const bool staged = PEERS && cta_r1 - cta_r0 <= kRowStage;  // (a separate instance: the plain one keeps its registers)
+  float *ystage = reinterpret_cast<float *>(smem + L.ystage);
+  auto emit = [&](uint32_t row, float v) {
+    if (staged) ystage[row - cta_r0] = v;
+    else put_y(a, y, row, v);
+  };
 
   for (uint32_t r = R0; r < R1; ++r) {
     if (r != R0) row_loads(r);
     if (e1 <= e0) {  // empty row
-      if (lane == 0) put_y(a, y, r, y_empty);
+      if (lane == 0) emit(r, y_empty);
       continue;
     }
     const uint32_t w0 = e0 & ~(kAlign - 1u), wn = w0 + kWin;
@@ -200,8 +214,11 @@ __global__ void __launch_bounds__(kRowNT, 1) k_matvec_row(DotArgs a, const float
     __syncwarp();  // the tables are rewritten by the next row
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-    if (lane == 0)
-      put_y(a, y, r, a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + a.bg * a.colsum[0]) : acc);
+    if (lane == 0) emit(r, a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + a.bg * a.colsum[0]) : acc);
+  }
+  if (staged) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < cta_r1 - cta_r0; i += kRowNT) put_y(a, y, cta_r0 + i, ystage[i]);
   }
   if (threadIdx.x == 0 && !ready) mbar_wait(xbar, 0);  // no CTA exits with the bulk copy in flight
 }
@@ -209,7 +226,7 @@ __global__ void __launch_bounds__(kRowNT, 1) k_matvec_row(DotArgs a, const float
 template <typename ColT, typename PtrT, bool CSER>
 int launch_row(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
   const size_t smem = row_layout(a.k, a.n, kRowNT / 32).total;
-  auto kern = k_matvec_row<ColT, PtrT, CSER>;
+  auto kern = a.npeer > 0 ? k_matvec_row<ColT, PtrT, CSER, true> : k_matvec_row<ColT, PtrT, CSER, false>;
   if (int rc_ = allow_max_smem(kern)) return rc_;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms(), a.m)));
   cudaLaunchConfig_t cfg = {};

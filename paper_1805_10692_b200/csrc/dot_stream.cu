@@ -37,7 +37,7 @@ constexpr uint32_t kSegRing = 256;     // segment bounds held per warp (8 batche
 // Dynamic shared memory: x first (so a gather is one scaled-index load), then the value table, the
 // per-warp flag tables and segment-bound rings, the x barrier.
 struct StreamSmem {
-  uint32_t wv, flag, opr, oir, bar, total;
+  uint32_t wv, flag, opr, oir, yb, bar, total;
 };
 __host__ __device__ __forceinline__ StreamSmem stream_layout(int64_t k, int64_t n, uint32_t warps, uint32_t flag_bytes,
                                                              uint32_t op_bytes, uint32_t oi_bytes) {
@@ -52,6 +52,7 @@ __host__ __device__ __forceinline__ StreamSmem stream_layout(int64_t k, int64_t 
   L.flag = take(warps * kStreamWin * flag_bytes);
   L.opr = take(warps * kSegRing * op_bytes);
   L.oir = take(warps * kSegRing * oi_bytes);
+  L.yb = take(warps * 128u);  // 32 results per warp, written out together
   L.bar = take(16u);
   L.total = o;
   return L;
@@ -207,7 +208,7 @@ __device__ __forceinline__ float prefix_at(const float g[8], int t) {
   return tt >= 8 ? g[7] : lo;
 }
 
-template <typename ColT, typename PtrT, bool CSER, typename FlagT, int D, int NT>
+template <typename ColT, typename PtrT, bool CSER, typename FlagT, int D, int NT, bool PEERS>
 __global__ void __launch_bounds__(NT, 1) k_matvec_stream(DotArgs a, const float *__restrict__ x,
                                                          float *__restrict__ y) {
   constexpr int kWarps = NT / 32;
@@ -342,6 +343,26 @@ __global__ void __launch_bounds__(NT, 1) k_matvec_stream(DotArgs a, const float 
     cgS = rr <= R1 ? row_s(rr) : 0u;
   };
   if (have_rows) group_load();
+  // Results leave the warp 32 rows at a time: lane j keeps y of the warp's row R0 + 32 g + j, and a full
+  // group (or the warp's last rows) is written as one coalesced store -- to y and, for the row-sharded
+  // exchange, to every peer's buffer (one 128 B NVLink store per 32 rows instead of 32 single-lane ones).
+  // (the 32 slots live in shared memory: a register held across the walk cost the CSER instance 6%; and
+  // the kernel without peers is its own instance that stores each result directly: the buffering cost it
+  // 1.5% on one GPU)
+  auto emit = [&](uint32_t row, float v) {
+    if (!PEERS) {
+      if (lane == 0) put_y(a, y, row, v);
+      return;
+    }
+    float *yb = reinterpret_cast<float *>(smem + L.yb) + wid * 32;
+    const uint32_t j = (row - R0) & 31u;
+    if (lane == 0) yb[j] = v;
+    if (j == 31u || row + 1 == R1) {
+      __syncwarp();
+      if (static_cast<uint32_t>(lane) <= j) put_y(a, y, row - j + lane, yb[lane]);
+      __syncwarp();
+    }
+  };
   // position the walk at the first non-empty row at or after r (empty rows are written here)
   auto row_init = [&]() {
     while (r < R1) {
@@ -359,7 +380,7 @@ __global__ void __launch_bounds__(NT, 1) k_matvec_stream(DotArgs a, const float 
         if (!CSER) slot_update(sb + lane - s0 + 1u);
         return;
       }
-      if (lane == 0) put_y(a, y, r, static_cast<float>(bgy));
+      emit(r, static_cast<float>(bgy));
       ++r;
     }
   };
@@ -477,7 +498,7 @@ __global__ void __launch_bounds__(NT, 1) k_matvec_stream(DotArgs a, const float 
         // the row ends in this window
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-        if (lane == 0) put_y(a, y, r, a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + bgy) : acc);
+        emit(r, a.bg != 0.0 ? static_cast<float>(static_cast<double>(acc) + bgy) : acc);
         ++r;
         row_init();
       }
@@ -491,7 +512,8 @@ template <typename ColT, typename PtrT, bool CSER, typename FlagT, int NT>
 int launch_stream(const DotArgs &a, const float *x, float *y, cudaStream_t st) {
   constexpr int D = (sizeof(ColT) == 4 || NT > 768) ? 2 : 3;
   const size_t smem = stream_layout(a.k, a.n, NT / 32, sizeof(FlagT), sizeof(PtrT), CSER ? a.oi_bits / 8 : 0).total;
-  auto kern = k_matvec_stream<ColT, PtrT, CSER, FlagT, D, NT>;
+  auto kern = a.npeer > 0 ? k_matvec_stream<ColT, PtrT, CSER, FlagT, D, NT, true>
+                          : k_matvec_stream<ColT, PtrT, CSER, FlagT, D, NT, false>;
   if (int rc_ = allow_max_smem(kern)) return rc_;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms(), ceil_div(a.m, NT / 32))));
   cudaLaunchConfig_t cfg = {};

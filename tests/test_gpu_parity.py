@@ -732,3 +732,34 @@ def test_stream_kernel_alphabets_modes_and_row_shapes(levels):
             for nt in (768, 896):
                 with force_path("matvec", "stream"), force_path("matvec_nt", nt):
                     assert np.array_equal(cd.dot(enc, x), want), (levels, bg, encode.__name__, nt)
+
+
+@pytest.mark.parametrize("path,m,n", [("stream", 150, 6000), ("row", 5000, 600), ("row", 90, 600)])
+def test_coalesced_peer_stores_stream_and_row_kernels(path, m, n):
+    """The peers instances of the stream kernel (32 results per warp in one store) and of the row kernel (a
+    CTA's contiguous rows staged, stored together): three emulated ranks, integer data -> every rank's
+    buffer holds exactly w @ x (uneven shards, rows that end mid-group, empty rows)."""
+    from paper_1805_10692_b200 import shard
+    from paper_1805_10692_b200._native import force_path
+
+    rng = np.random.default_rng(m + n)
+    w = rng.choice(np.arange(-3.0, 4.0), size=(m, n), p=[0.03, 0.04, 0.05, 0.76, 0.05, 0.04, 0.03])
+    w[1] = 0.0
+    w[m - 1] = 0.0
+    x = rng.integers(-2, 3, size=n).astype(np.float64)
+    xt = torch.from_numpy(x.astype(np.float32)).cuda()
+    want = torch.from_numpy((w @ x).astype(np.float32)).cuda()
+    ranks = 3
+    for encode in (cd.encode_cer, cd.encode_cser):
+        full = encode(w)
+        bounds = [0, m // 5, m // 5 + m // 2, m]
+        bufs = [torch.full((m,), float("nan"), device="cuda") for _ in range(ranks)]
+        with force_path("matvec", path):
+            for r in range(ranks):
+                local = shard.slice_rows(full, bounds[r], bounds[r + 1])
+                peers = torch.tensor([b.data_ptr() for q, b in enumerate(bufs) if q != r], dtype=torch.int64,
+                                     device="cuda")
+                cd.dot_device(local, xt, out=bufs[r][bounds[r]:bounds[r + 1]], peers=peers, peer_offset=bounds[r])
+        torch.cuda.synchronize()
+        for b in bufs:
+            assert torch.equal(b, want), (path, encode.__name__)
