@@ -53,6 +53,7 @@ struct Ctrl {
   int pad;
   double background;         // omega[0]
   unsigned long long max_stat[3];  // largest per-row nnz, CER segments, CSER segments
+  unsigned long long totals[3];    // nnz, CER segments, CSER segments (= the scans' last entries)
 };
 
 struct FastWs {
@@ -727,7 +728,10 @@ __global__ void __launch_bounds__(1024) k_scan_rows(int64_t m, FastWs ws) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mm = max(mm, static_cast<uint64_t>(__shfl_xor_sync(0xffffffffu, mm, o)));
       wsum[j][lane] = wi - w;  // exclusive warp offsets
-      if (lane == 31) ws.scan[j * (m + 1) + m] = wi;
+      if (lane == 31) {
+        ws.scan[j * (m + 1) + m] = wi;
+        ws.ctrl->totals[j] = wi;  // read back with the rest of the control block: one copy, not four
+      }
       if (lane == 0) ws.ctrl->max_stat[j] = mm;
     }
   }
@@ -1110,8 +1114,9 @@ int encode_plan(const void *w, int dtype, int64_t m, int64_t n, int64_t ldw, int
   if (workspace == nullptr || workspace_bytes < need)
     return fail(CERDOT_E_WORKSPACE, "encode workspace too small: need " + std::to_string(need) + " bytes");
   FastWs ws = carve(workspace, m, n);
-  CERDOT_CUDA_CHECK(cudaMemsetAsync(ws.gkey, 0, sizeof(unsigned long long) * kGlobalCap, st));
-  CERDOT_CUDA_CHECK(cudaMemsetAsync(ws.gcnt, 0, sizeof(unsigned long long) * kGlobalCap, st));
+  // the key and count tables are adjacent in the workspace (carve): one memset
+  CERDOT_CUDA_CHECK(cudaMemsetAsync(ws.gkey, 0,
+                                    reinterpret_cast<char *>(ws.gcnt + kGlobalCap) - reinterpret_cast<char *>(ws.gkey), st));
   CERDOT_CUDA_CHECK(cudaMemsetAsync(ws.ctrl, 0, sizeof(Ctrl), st));
   int rc = dtype == CERDOT_F32 ? launch_hist<float>(w, m, n, ldw, ws, st) : launch_hist<double>(w, m, n, ldw, ws, st);
   if (rc) return rc;
@@ -1128,12 +1133,9 @@ int encode_plan(const void *w, int dtype, int64_t m, int64_t n, int64_t ldw, int
   k_scan_rows<<<1, 1024, 0, st>>>(m, ws);
   CERDOT_LAUNCH_CHECK();
   Ctrl ctrl{};
-  uint64_t totals[3];
   CERDOT_CUDA_CHECK(cudaMemcpyAsync(&ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-  for (int j = 0; j < 3; ++j)
-    CERDOT_CUDA_CHECK(
-        cudaMemcpyAsync(&totals[j], ws.scan + j * (m + 1) + m, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   CERDOT_CUDA_CHECK(cudaStreamSynchronize(st));
+  const unsigned long long *totals = ctrl.totals;
   if (ctrl.overflow)  // alphabet too large for the on-chip tables: sort-based path (encode_sort.cu)
     return encode_sort_plan(w, dtype, m, n, ldw, bg_mode, bg_value, workspace, workspace_bytes, info, st);
   const unsigned int k = ctrl.k;
