@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define CERDOT_ABI_VERSION 2
+#define CERDOT_ABI_VERSION 3
 
 typedef enum {
   CERDOT_OK = 0,

@@ -138,7 +138,7 @@ def lib() -> ctypes.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.cerdot_abi_version() != 2:
+        if L.cerdot_abi_version() != 3:
             raise ImportError("libcerdot ABI version mismatch")
         _lib = L
     return _lib

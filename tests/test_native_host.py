@@ -31,7 +31,7 @@ def test_library_exports_every_header_symbol():
     assert len(names) >= 11
     for name in names:
         assert hasattr(L, name), name
-    assert L.cerdot_abi_version() == 2
+    assert L.cerdot_abi_version() == 3
 
 
 def test_index_bitwidth_matches_reference_table():
