@@ -28,7 +28,7 @@ for name, b in cases:
     xs = [torch.from_numpy(x).cuda() for _ in range(rot)]
     ys = [torch.empty((cfg.m, b), device="cuda") for _ in range(rot)]
     ref = None
-    for path, split, nt in [("flat", 0, 0)] + [("tiled", s, t) for t in (128, 256) for s in (1, 2, 4, 8)]:
+    for path, split, nt in [("flat", 0, 0)] + [("tiled", s, t) for t in [int(v) for v in os.environ.get("MM_TILES", "128 256").split()] for s in (1, 2, 4, 8)]:
         with force_path("matmat", path), force_path("matmat_split", split), force_path("matmat_tile", nt):
             for i in range(rot):
                 cd.dot_device(copies[i], xs[i], out=ys[i])
