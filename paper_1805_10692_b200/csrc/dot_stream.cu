@@ -437,22 +437,22 @@ __global__ void __launch_bounds__(NT, 1) k_matvec_stream(DotArgs a, const float 
             Flags<FlagT> fl;
             fl.load(myflag_s);
             if (fl.any()) Flags<FlagT>::clear(myflag_s);
-            uint32_t fm = fl.mask();
-            const uint32_t F = __ballot_sync(kFull, fm != 0u);
+            const uint32_t F = __ballot_sync(kFull, fl.any());
+            // walk the lane's 8 entries in order (static positions: no prefix select, no per-flag loop; a
+            // segment-dense row tail holds several flags per lane)
             float ghead = 0.f, glast = 0.f, vlast = 0.f, accl = 0.f;
             bool have = false;
-            while (__any_sync(kFull, fm != 0u)) {
-              if (fm != 0u) {
-                const uint32_t b = static_cast<uint32_t>(__ffs(static_cast<int>(fm))) - 1u;
-                fm &= fm - 1u;
-                const float v = lds_f32(wv_s + 4u * fl.at(b));
-                const float gb = prefix_before(g, b);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+              const uint32_t slot = fl.at(b);
+              if (slot != 0u) {
+                const float gb = b ? g[b - 1] : 0.f;
                 if (have)
                   accl = fmaf(vlast, gb - glast, accl);
                 else
                   ghead = gb;
                 have = true;
-                vlast = v;
+                vlast = lds_f32(wv_s + 4u * slot);
                 glast = gb;
               }
             }
