@@ -9,14 +9,21 @@
 //   * colI goes global -> registers (16 B per lane per window), D windows in flight in a statically
 //     indexed register ring; a warp's rows are contiguous in colI, so the ring is one linear stream and a
 //     window that straddles a row boundary is simply walked once per row;
-//   * segments never meet across lanes.  The lanes that hold the current batch of 32 segment bounds mark
-//     each non-empty segment's first entry in a 256-slot per-warp flag table with the segment's value slot;
-//     a lane reads the 8 flags of its 8 entries, sums its entries fragment by fragment (a fragment = the
-//     part of a segment inside one lane, <= 8 entries) and multiplies each fragment once by its segment's
-//     value: sum_seg v * S(seg) = sum_fragments v * S(fragment).  The value in force at a lane's first
-//     entry comes from the nearest flagged lane below it (one shuffle), or from the previous window;
-//   * windows in which no segment starts (the frequent values' long segments) touch neither the table
-//     nor the shuffle unit: eight gathers, eight adds, one fma.
+//   * segment bounds (omegaPtr, omegaI) are one linear stream per warp too, copied 8 batches of 32 ahead
+//     into a per-warp ring by cp.async; row bounds are held lane-parallel and read by shuffle (a pending
+//     row-bound load shared a scoreboard with the colI ring: profiles/r02_stream_notes.txt);
+//   * segments never meet across lanes: a lane sums its 8 entries fragment by fragment (a fragment = the
+//     part of a segment inside one lane) and multiplies each fragment once by its segment's value,
+//     sum_seg v * S(seg) = sum_fragments v * S(fragment).  Up to four segment starts in a window are
+//     broadcast one by one from the lanes that hold the segments (one shuffle, one value read, an
+//     in-register prefix select each); more starts (a row's segment-dense tail) are marked in a 256-slot
+//     per-warp flag table with the segment's value slot, and every lane walks the 8 flags of its entries
+//     in order.  The value in force at a lane's first entry is warp-uniform state (the few-starts path)
+//     or comes from the nearest flagged lane below (one shuffle);
+//   * windows in which no segment starts touch neither the table nor the shuffle unit: eight gathers,
+//     eight adds, one fma.
+// 28 warps per SM at <= 72 registers, two windows in flight.  The kernel is bound by instruction issue
+// (~195 per window at 0.80 per scheduler per cycle), not by the shared-memory pipe.
 // Summation order (stated for the 1e-5 bar): fp32 fragment sums in colI order, one fp32 fma per fragment
 // into a per-lane accumulator, lanes combined by an xor butterfly per row.  Deterministic.
 #include <cuda_runtime.h>
