@@ -879,11 +879,14 @@ __global__ void __launch_bounds__(kRowThreads) k_row_fill(int64_t m, int64_t n, 
   }
 }
 
-// CTA per row, u8 rank grid, n a multiple of 16: each warp first compacts the non-zero ranks of its column
-// slab into a shared list of (column << 8 | rank) entries in column order (16 ranks per lane per load,
-// one warp scan per 512 columns), so the per-rank counting and the stable scatter walk only the row's
-// entries instead of every column (a 91%-zero fc layer: 11x fewer steps; 130 -> ~45 us on AlexNet fc6).
-template <typename ColT, bool CSER>
+// CTA per row, u8 rank grid, n a multiple of 16: a warp compacts the non-zero ranks of its column slab into
+// a shared list of (column << 8 | rank) entries in column order (16 ranks per lane per load, one warp scan
+// per 512 columns), so the stable scatter walks only the row's entries instead of every column.
+//   CHUNKED = false (sparse rows): the whole slab is listed once, counting on the way (a 91%-zero fc layer:
+//     11x fewer scatter steps; 130 -> 56 us on AlexNet fc6);
+//   CHUNKED = true (any density, 2 KB of list per warp): a counting pass, then 512 columns at a time are
+//     listed and scattered (the 32768^2 layer at 30%: a third of the scatter steps).
+template <typename ColT, bool CSER, bool CHUNKED>
 __global__ void __launch_bounds__(kRowThreads) k_row_fill_compact(int64_t m, int64_t n, FastWs ws, uint32_t cap,
                                                                   ColT *__restrict__ col, void *omega_ptr, int op_bits,
                                                                   void *omega_index, int oi_bits) {
@@ -907,9 +910,9 @@ __global__ void __launch_bounds__(kRowThreads) k_row_fill_compact(int64_t m, int
     __syncthreads();
     const uint8_t *rr = ranks + row * n;
     const int64_t c_begin = wid * slab, c_end = min64(n, c_begin + slab);
-    // ---- compact: the warp's non-zero ranks, in column order
-    uint32_t nzw = 0;
-    for (int64_t c0 = c_begin; c0 < c_end; c0 += 512) {
+    // one 512-column step: the non-zero ranks, listed from `base` in column order (LIST) and / or counted
+    // per rank (COUNT); returns how many there were
+    auto step = [&](int64_t c0, uint32_t base, bool do_list, bool do_count) -> uint32_t {
       const int64_t c = c0 + 16 * lane;
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
       if (c < c_end) v = *reinterpret_cast<const uint4 *>(rr + c);  // n % 16 == 0: whole vectors
@@ -922,13 +925,14 @@ __global__ void __launch_bounds__(kRowThreads) k_row_fill_compact(int64_t m, int
         mine += __popc(nib[j]);
       }
       uint32_t incl = mine;
+      if (do_list) {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
       }
-      uint32_t at = nzw + incl - mine;
-      nzw += __shfl_sync(0xffffffffu, incl, 31);
+      uint32_t at = base + incl - mine;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint32_t mk = nib[j];
@@ -936,11 +940,15 @@ __global__ void __launch_bounds__(kRowThreads) k_row_fill_compact(int64_t m, int
           const int b = __ffs(static_cast<int>(mk)) - 1;
           mk &= mk - 1u;
           const uint32_t rk = (wv4[j] >> (8 * b)) & 0xffu;
-          list[at++] = (static_cast<uint32_t>(c + 4 * j + b) << 8) | rk;
-          atomicAdd(&wc[wid * k + rk], 1u);
+          if (do_list) list[at++] = (static_cast<uint32_t>(c + 4 * j + b) << 8) | rk;
+          if (do_count) atomicAdd(&wc[wid * k + rk], 1u);
         }
       }
-    }
+      return do_list ? __shfl_sync(0xffffffffu, incl, 31) : 0u;
+    };
+    // ---- count (and, for sparse rows, list the whole slab)
+    uint32_t nzw = 0;
+    for (int64_t c0 = c_begin; c0 < c_end; c0 += 512) nzw += step(c0, nzw, !CHUNKED, true);
     __syncthreads();
     // per rank: total count and per-warp exclusive offsets
     for (unsigned int q = threadIdx.x; q < k; q += blockDim.x) {
@@ -981,18 +989,29 @@ __global__ void __launch_bounds__(kRowThreads) k_row_fill_compact(int64_t m, int
         store_index(omega_ptr, op_bits, s0 + q, end);  // segment s0 + q - 1 ends here
       }
     }
-    // stable scatter over the warp's entries: warp lists are column-ordered, lanes ordered inside a step
-    for (uint32_t i0 = 0; i0 < nzw; i0 += 32) {
-      const uint32_t e = i0 + lane < nzw ? list[i0 + lane] : 0u;
-      const unsigned int rk = e & 0xffu;
-      const unsigned int peers = __match_any_sync(0xffffffffu, rk);
-      if (rk != 0) {
-        const uint64_t pos = e0 + excl[rk] + wc[wid * k + rk] + __popc(peers & lt);
-        col[pos] = static_cast<ColT>(e >> 8);
+    // stable scatter over listed entries: warp lists are column-ordered, lanes ordered inside a step
+    auto scatter = [&](uint32_t count) {
+      for (uint32_t i0 = 0; i0 < count; i0 += 32) {
+        const uint32_t e = i0 + lane < count ? list[i0 + lane] : 0u;
+        const unsigned int rk = e & 0xffu;
+        const unsigned int peers = __match_any_sync(0xffffffffu, rk);
+        if (rk != 0) {
+          const uint64_t pos = e0 + excl[rk] + wc[wid * k + rk] + __popc(peers & lt);
+          col[pos] = static_cast<ColT>(e >> 8);
+        }
+        __syncwarp();
+        if (rk != 0 && lane == __ffs(peers) - 1) wc[wid * k + rk] += __popc(peers);
+        __syncwarp();
       }
-      __syncwarp();
-      if (rk != 0 && lane == __ffs(peers) - 1) wc[wid * k + rk] += __popc(peers);
-      __syncwarp();
+    };
+    if (CHUNKED) {
+      for (int64_t c0 = c_begin; c0 < c_end; c0 += 512) {
+        const uint32_t got = step(c0, 0u, true, false);
+        __syncwarp();
+        scatter(got);
+      }
+    } else {
+      scatter(nzw);
     }
     __syncthreads();
   }
@@ -1063,26 +1082,29 @@ template <typename ColT, typename RankT>
 int launch_fill(int64_t m, int64_t n, const FastWs &ws, unsigned int k, int64_t max_row_nnz, int64_t nnz, bool cser, void *col,
                 void *op, int op_bits, void *oi, int oi_bits, cudaStream_t st) {
   const size_t smem = (kRowWarps + 3) * static_cast<size_t>(k) * sizeof(unsigned int);
-  // u8 ranks, whole 16 B vectors per row, columns that fit 24 bits, at most 20% non-zero (denser rows gain
-  // nothing from compaction: the 32768^2 layer at 30% ran 9.0 vs 7.3 ms): the compacting kernel, its
-  // per-warp entry lists sized by the longest row (a warp's slab cannot hold more), four CTAs per SM
-  if (sizeof(RankT) == 1 && (n % 16) == 0 && n < (int64_t(1) << 24) && nnz <= m * n / 5) {
+  // u8 ranks, whole 16 B vectors per row, columns that fit 24 bits: the compacting kernel.  Sparse rows
+  // (<= 20% non-zero) whose per-warp lists fit (sized by the longest row: a warp's slab cannot hold more)
+  // are listed whole; otherwise 512 columns at a time (2 KB of list per warp).
+  if (sizeof(RankT) == 1 && (n % 16) == 0 && n < (int64_t(1) << 24)) {
     const int64_t slab = ceil_div(ceil_div(n, kRowWarps), 512) * 512;
-    const uint32_t cap = static_cast<uint32_t>(std::min<int64_t>(slab, std::max<int64_t>(max_row_nnz, 1)));
+    const uint32_t cap_whole = static_cast<uint32_t>(std::min<int64_t>(slab, std::max<int64_t>(max_row_nnz, 1)));
+    const bool whole = nnz <= m * n / 5 && smem + sizeof(uint32_t) * kRowWarps * static_cast<size_t>(cap_whole) <= 56 * 1024;
+    const uint32_t cap = whole ? cap_whole : 512u;
     const size_t smem_c = smem + sizeof(uint32_t) * kRowWarps * static_cast<size_t>(cap);
-    if (smem_c <= 56 * 1024) {
-      auto goc = [&](auto kern) -> int {
-        CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_c)));
-        int per_sm = 0;
-        CERDOT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, smem_c));
-        const int grid = static_cast<int>(std::min<int64_t>(m, static_cast<int64_t>(num_sms()) * std::max(per_sm, 1)));
-        kern<<<grid, kRowThreads, smem_c, st>>>(m, n, ws, cap, static_cast<ColT *>(col), op, op_bits, oi, oi_bits);
-        return CERDOT_OK;
-      };
-      if (int rc = cser ? goc(k_row_fill_compact<ColT, true>) : goc(k_row_fill_compact<ColT, false>)) return rc;
-      CERDOT_LAUNCH_CHECK();
+    auto goc = [&](auto kern) -> int {
+      CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_c)));
+      int per_sm = 0;
+      CERDOT_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, smem_c));
+      const int grid = static_cast<int>(std::min<int64_t>(m, static_cast<int64_t>(num_sms()) * std::max(per_sm, 1)));
+      kern<<<grid, kRowThreads, smem_c, st>>>(m, n, ws, cap, static_cast<ColT *>(col), op, op_bits, oi, oi_bits);
       return CERDOT_OK;
-    }
+    };
+    int rc;
+    if (whole) rc = cser ? goc(k_row_fill_compact<ColT, true, false>) : goc(k_row_fill_compact<ColT, false, false>);
+    else rc = cser ? goc(k_row_fill_compact<ColT, true, true>) : goc(k_row_fill_compact<ColT, false, true>);
+    if (rc) return rc;
+    CERDOT_LAUNCH_CHECK();
+    return CERDOT_OK;
   }
   auto go = [&](auto kern) -> int {
     CERDOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
