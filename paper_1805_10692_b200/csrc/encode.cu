@@ -1036,7 +1036,7 @@ int launch_hist(const void *w, int64_t m, int64_t n, int64_t ldw, const FastWs &
   const bool vec_ok = (ldw == n) && (reinterpret_cast<uintptr_t>(w) % 16 == 0);
   if (sizeof(T) == 4 && vec_ok && total % 4 == 0) {  // fp32, contiguous: integer keys on chip
     const int64_t nvec = total / 4;
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nvec, 256 * 8), num_sms() * 8)));
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nvec, 256 * 8), num_sms() * 6)));
     k_value_hist_f32<<<grid, 256, 0, st>>>(static_cast<const float4 *>(w), nvec, ws);
     CERDOT_LAUNCH_CHECK();
     return CERDOT_OK;
