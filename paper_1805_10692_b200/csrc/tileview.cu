@@ -517,6 +517,27 @@ __global__ void __launch_bounds__(256) k_tv_reduce(const float *__restrict__ par
                                                    float *__restrict__ y, int64_t ldy, float *const *ypeer, int npeer,
                                                    int64_t ypeer_off) {
   const int64_t total = m * batch;
+  if (npeer == 0 && (batch & 3) == 0 && (ldp & 3) == 0 && (ldy & 3) == 0 &&
+      ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(part)) & 15) == 0) {  // four columns per thread
+    const int64_t q = batch >> 2;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m * q;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      const int64_t r = i / q, c = (i - r * q) << 2;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint32_t z = 0; z < splits; ++z) {
+        const float4 p = *reinterpret_cast<const float4 *>(part + (static_cast<int64_t>(z) * m + r) * ldp + c);
+        v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
+      }
+      if (bg != 0.0) {
+        v.x = static_cast<float>(static_cast<double>(v.x) + bg * colsum[c]);
+        v.y = static_cast<float>(static_cast<double>(v.y) + bg * colsum[c + 1]);
+        v.z = static_cast<float>(static_cast<double>(v.z) + bg * colsum[c + 2]);
+        v.w = static_cast<float>(static_cast<double>(v.w) + bg * colsum[c + 3]);
+      }
+      *reinterpret_cast<float4 *>(y + r * ldy + c) = v;
+    }
+    return;
+  }
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t r = i / batch, c = i - r * batch;
@@ -827,7 +848,7 @@ int matmat_tiled(const cerdot_matrix *mat, const float *x, int64_t ldx, int64_t 
   if (rc) return rc;
   CERDOT_LAUNCH_CHECK();
   if (splits > 1) {
-    const int rgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(mat->m * batch, 256), num_sms() * 8)));
+    const int rgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(mat->m * batch, 1024), num_sms() * 8)));
     k_tv_reduce<<<rgrid, 256, 0, st>>>(a.part, ldp, static_cast<uint32_t>(splits), mat->m, batch, a.bg, colsum, y, ldy,
                                         a.ypeer, a.npeer, a.ypeer_off);
     CERDOT_LAUNCH_CHECK();
