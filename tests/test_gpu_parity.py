@@ -193,8 +193,8 @@ def test_u32_column_indices(kernel_path, path):
 
 
 def test_long_rows_default_to_run_kernel_and_match_oracle():
-    """Rows of >= 4096 entries take the run kernel by default (colI ring across rows, segment batches
-    that close several times inside one window, CER padding); integer alphabet -> bitwise, real -> 1e-5."""
+    """Rows of >= 4096 entries take the long-row (stream) kernel by default (colI ring across rows, several
+    segment batches inside one window, CER padding); integer alphabet -> bitwise, real -> 1e-5."""
     rng = np.random.default_rng(21)
     m, n = 96, 20000
     levels = np.arange(-12, 13, dtype=np.float64)
@@ -320,7 +320,7 @@ def test_wide_alphabets_up_to_fast_limit():
 @pytest.mark.parametrize("path", ["tile", "window", "run", "stream", "row"])
 @pytest.mark.parametrize("name", ["oracle", "alexnet-fc6", "resnet-conv"])
 def test_matvec_paths_agree_with_oracle(kernel_path, config_goldens, name, path):
-    """Every mat-vec kernel (CTA-tile TMA pipeline, warp-window kernel, 32-warp run kernel) meets the bar."""
+    """Every mat-vec kernel (CTA-tile TMA pipeline, warp-window, run, stream and row kernels) meets the bar."""
     kernel_path("matvec", path)
     meta, ys = config_goldens
     w, _ = synth.make_layer(name)
